@@ -1,0 +1,151 @@
+/*
+ * pdas_b200.h -- C-ABI of the B200-native PDAS / Egidi-Maponi hot path.
+ *
+ * This is the drop-in boundary for the reference's kernel core: the function
+ * table that adascale/_core.py:10-16 exposes as `kernels` (implemented by
+ * adascale/_kernels.pyx, the compiled core).  Every entry point below names
+ * the reference routine it replaces.  The host side (paper_1502_03543_b200,
+ * Python) binds it with ctypes exactly as the reference binds its Cython core.
+ *
+ * Conventions
+ *   - fp64 throughout; every matrix is column-contiguous, element (i,j) at
+ *     j*rows + i (reference linalg.py:1-7).
+ *   - all array pointers are DEVICE pointers on the current CUDA device;
+ *     `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *   - launches are asynchronous on `stream`; data-dependent results
+ *     (Cholesky fail column, cascade breakdown step) are written to a device
+ *     word the caller reads after synchronising.
+ *   - arithmetic is bitwise-identical to the reference compiled core (fixed
+ *     pairwise tree, no fused multiply-add, sequential orders of gram /
+ *     Cholesky / triangular solves).
+ *   - return value: PDAS_OK or a negative PDAS_ERR_*; pdas_last_error()
+ *     gives the message of the last failure on the calling thread.
+ */
+#ifndef PDAS_B200_H
+#define PDAS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PDAS_ABI_VERSION 1
+
+#define PDAS_OK 0
+#define PDAS_ERR_ARG (-1)         /* bad argument / shape */
+#define PDAS_ERR_CUDA (-2)        /* CUDA runtime error (message in pdas_last_error) */
+#define PDAS_ERR_UNSUPPORTED (-3) /* size outside the compiled configurations */
+#define PDAS_ERR_NOMEM (-4)
+
+/* Device-resident state of one PDAS iteration (solver.py:152-279).  Written
+ * by the pdas_iter_* kernels, read back by the host once per iteration. */
+typedef struct PdasIterState {
+    int64_t chol_fail;       /* -1 ok, else failing column (linalg.py:120-122)   */
+    int64_t blocking;        /* ratio-test argmin in [0,2n): j = x_j, n+j = s_j    */
+    int32_t cascade_fail;    /* 0 or 1-based breakdown step (normal.py:172-173)  */
+    uint32_t interior_flags; /* bit0 x NaN, bit1 x<=0, bit2 s NaN, bit3 s<=0       */
+    int32_t nonfinite;       /* 1: dx, dy or ds has a non-finite entry (:229-235)  */
+    int32_t stepped;         /* 1: x, y, s were updated this iteration             */
+    int32_t fallback;        /* 1: dy came from the direct solve (:161-165)       */
+    int32_t reserved;
+    double alpha, gap, pobj, dobj, r_primal, r_dual, r_comp, min_ratio;
+} PdasIterState;
+
+int pdas_abi_version(void);
+const char* pdas_last_error(void);
+/* SM count and compute capability of the current device. */
+int pdas_device_info(int* sm_count, int* cc_major, int* cc_minor);
+/* Largest m the rank-one cascade kernels are compiled for. */
+int64_t pdas_cascade_max_m(void);
+
+/* ---- kernel table (adascale/_kernels.pyx) --------------------------------- */
+
+/* dot_tree, _kernels.pyx:55-71.  *out_dev = tree_i u[i*su]*v[i*sv], n >= 1. */
+int pdas_dot_tree(const double* u, int64_t su, const double* v, int64_t sv, int64_t n,
+                  double* out_dev, void* stream);
+
+/* mat_vec, _kernels.pyx:74-88.  out[i] = tree_k a[i,k]*x[k]; a is m x n. */
+int pdas_mat_vec(const double* a, int64_t m, int64_t n, const double* x, double* out,
+                 void* stream);
+
+/* mat_t_vec, _kernels.pyx:91-105.  out[j] = tree_i a[i,j]*y[i]. */
+int pdas_mat_t_vec(const double* a, int64_t m, int64_t n, const double* y, double* out,
+                   void* stream);
+
+/* gram, _kernels.pyx:108-123.  g (m x m) = A A^T, sequential k, mirrored. */
+int pdas_gram(const double* a, int64_t m, int64_t n, double* g, void* stream);
+
+/* scaled_gram, _kernels.pyx:126-141.  g = A diag(d) A^T (w = a[j,k]*d[k]). */
+int pdas_scaled_gram(const double* a, int64_t m, int64_t n, const double* d, double* g,
+                     void* stream);
+
+/* cholesky_factor, _kernels.pyx:144-171.  low (nn x nn) is fully written
+ * (zeros above the diagonal and in columns >= the failing one);
+ * *fail_dev = -1 on success, else the first failing column. */
+int pdas_cholesky_factor(const double* g, int64_t nn, double eps_rel, double* low,
+                         int64_t* fail_dev, void* stream);
+
+/* cholesky_solve_many, _kernels.pyx:174-193.  Solves (L L^T) X = B in place
+ * on x (m x k). */
+int pdas_cholesky_solve_many(const double* low, int64_t m, double* x, int64_t k, void* stream);
+
+/* build_v, _kernels.pyx:196-202.  v[i] = a[i,l0]*(dl - 1). */
+int pdas_build_v(const double* a, int64_t m, int64_t l0, double dl, double* v, void* stream);
+
+/* sweep_phase1, _kernels.pyx:205-218.  inner[k] = tree(v, cols[:,k]), k in [k0,k1). */
+int pdas_sweep_phase1(const double* cols, int64_t m, const double* v, double* inner, int64_t k0,
+                      int64_t k1, void* stream);
+
+/* sweep_phase2, _kernels.pyx:221-231.  cols[:,k] -= (inner[k]/denom)*cols[:,l0]. */
+int pdas_sweep_phase2(double* cols, int64_t m, int64_t l0, const double* inner, double denom,
+                      int64_t k0, int64_t k1, void* stream);
+
+/* solve_sweeps / _cascade, _kernels.pyx:234-291.  The full Egidi-Maponi
+ * cascade in place on cols (m x (n+1)) = [Y | x]; *fail_dev = 0 or the
+ * 1-based breakdown step.  `inner` and `v` are accepted for interface parity
+ * (scratch, contents unspecified afterwards, as in the reference);
+ * `workers` is accepted and ignored (results never depend on it). */
+int pdas_solve_sweeps(double* cols, const double* a, const double* d, double* inner, double* v,
+                      int64_t m, int64_t n, int workers, int32_t* fail_dev, void* stream);
+
+/* ---- fused per-iteration path (adascale/solver.py) ------------------------- */
+
+/* Reset *state (all zero, chol_fail = -1). */
+int pdas_iter_reset(PdasIterState* state, void* stream);
+
+/* scaling_diag + check_interior, solver.py:142-145 / model.py:116-119:
+ * d = x/s, interior flags into state. */
+int pdas_iter_scaling(const double* x, const double* s, int64_t n, double* d,
+                      PdasIterState* state, void* stream);
+
+/* compute_directions tail + step_length, solver.py:166-189: t = A^T dy,
+ * ds = -t, dx = d*t - x, residuals, finiteness, ratio test, alpha and the
+ * step decision.  Needs state->cascade_fail / chol_fail already final. */
+int pdas_iter_directions(const double* a, int64_t m, int64_t n, const double* dy,
+                         const double* d, const double* x, const double* s, double* dx,
+                         double* ds, double rho, PdasIterState* state, void* stream);
+
+/* x += alpha*dx, y += alpha*dy, s += alpha*ds when state->stepped (solver.py:257-259). */
+int pdas_iter_update(double* x, double* y, double* s, const double* dx, const double* dy,
+                     const double* ds, int64_t n, int64_t m, const PdasIterState* state,
+                     void* stream);
+
+/* gap = tree(x,s), pobj = tree(c,x), dobj = tree(b,y)  (solver.py:192-194, 246-247). */
+int pdas_iter_objectives(const double* x, const double* s, const double* c, const double* b,
+                         const double* y, int64_t n, int64_t m, PdasIterState* state,
+                         void* stream);
+
+/* ---- diagnostics ----------------------------------------------------------- */
+
+/* Sustained separately-rounded fp64 multiply+add rate probe (the cascade's
+ * instruction mix); *ops = number of fp64 operations the launch performs.
+ * Time it with events on `stream` to get the roofline denominator. */
+int pdas_probe_fp64(double* sink, int64_t iters, int64_t* ops, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PDAS_B200_H */

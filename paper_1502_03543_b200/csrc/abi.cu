@@ -1,0 +1,224 @@
+// abi.cu -- extern "C" entry points declared in include/pdas_b200.h.
+// Thin: validate arguments, allocate stream-ordered scratch, launch, map
+// CUDA errors to PDAS_ERR_CUDA with a per-thread message.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "pdas_internal.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int set_err(int code, const char* what) {
+    snprintf(g_err, sizeof g_err, "%s", what);
+    return code;
+}
+
+int check_cuda(int rc, const char* where) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        snprintf(g_err, sizeof g_err, "%s: %s", where, cudaGetErrorString(e));
+        return PDAS_ERR_CUDA;
+    }
+    if (rc == PDAS_ERR_UNSUPPORTED) return set_err(rc, where);
+    if (rc == PDAS_ERR_ARG) return set_err(rc, where);
+    if (rc != PDAS_OK) {
+        snprintf(g_err, sizeof g_err, "%s: error %d", where, rc);
+        return rc;
+    }
+    return PDAS_OK;
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+template <class T>
+int scratch(T** p, size_t count, cudaStream_t st) {
+    *p = nullptr;
+    if (count == 0) return PDAS_OK;
+    if (cudaMallocAsync((void**)p, count * sizeof(T), st) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(PDAS_ERR_NOMEM, "cudaMallocAsync failed");
+    }
+    return PDAS_OK;
+}
+
+}  // namespace
+
+using pdas::idx_t;
+
+extern "C" {
+
+int pdas_abi_version(void) { return PDAS_ABI_VERSION; }
+
+const char* pdas_last_error(void) { return g_err; }
+
+int pdas_device_info(int* sm_count, int* cc_major, int* cc_minor) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return check_cuda(PDAS_OK, "cudaGetDevice");
+    if (sm_count) cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, dev);
+    if (cc_major) cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (cc_minor) cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+    return check_cuda(PDAS_OK, "pdas_device_info");
+}
+
+int64_t pdas_cascade_max_m(void) { return pdas::cascade_supported_m(); }
+
+int pdas_dot_tree(const double* u, int64_t su, const double* v, int64_t sv, int64_t n,
+                  double* out_dev, void* stream) {
+    if (n < 1) return set_err(PDAS_ERR_ARG, "dot_tree requires length >= 1");
+    return check_cuda(pdas::launch_dot_tree(u, su, v, sv, n, out_dev, S(stream)), "dot_tree");
+}
+
+int pdas_mat_vec(const double* a, int64_t m, int64_t n, const double* x, double* out,
+                 void* stream) {
+    if (m < 0 || n < 1) return set_err(PDAS_ERR_ARG, "mat_vec: bad shape");
+    double* work = nullptr;
+    int rc = scratch(&work, (size_t)pdas::mat_vec_scratch(m, n), S(stream));
+    if (rc) return rc;
+    rc = pdas::launch_mat_vec(a, m, n, x, out, work, S(stream));
+    if (work) cudaFreeAsync(work, S(stream));
+    return check_cuda(rc, "mat_vec");
+}
+
+int pdas_mat_t_vec(const double* a, int64_t m, int64_t n, const double* y, double* out,
+                   void* stream) {
+    if (m < 1 || n < 0) return set_err(PDAS_ERR_ARG, "mat_t_vec: bad shape");
+    return check_cuda(pdas::launch_mat_t_vec(a, m, n, y, out, S(stream)), "mat_t_vec");
+}
+
+int pdas_gram(const double* a, int64_t m, int64_t n, double* g, void* stream) {
+    if (m < 1 || n < 0) return set_err(PDAS_ERR_ARG, "gram: bad shape");
+    return check_cuda(pdas::launch_gram(a, m, n, nullptr, g, S(stream)), "gram");
+}
+
+int pdas_scaled_gram(const double* a, int64_t m, int64_t n, const double* d, double* g,
+                     void* stream) {
+    if (m < 1 || n < 0 || d == nullptr) return set_err(PDAS_ERR_ARG, "scaled_gram: bad args");
+    return check_cuda(pdas::launch_gram(a, m, n, d, g, S(stream)), "scaled_gram");
+}
+
+int pdas_cholesky_factor(const double* g, int64_t nn, double eps_rel, double* low,
+                         int64_t* fail_dev, void* stream) {
+    if (nn < 1) return set_err(PDAS_ERR_ARG, "cholesky_factor: bad shape");
+    double* work = nullptr;
+    int rc = scratch(&work, (size_t)pdas::cholesky_work_doubles(nn), S(stream));
+    if (rc) return rc;
+    rc = pdas::launch_cholesky(g, nn, eps_rel, low, fail_dev, work, S(stream));
+    cudaFreeAsync(work, S(stream));
+    return check_cuda(rc, "cholesky_factor");
+}
+
+int pdas_cholesky_solve_many(const double* low, int64_t m, double* x, int64_t k, void* stream) {
+    if (m < 1 || k < 0) return set_err(PDAS_ERR_ARG, "cholesky_solve_many: bad shape");
+    double* work = nullptr;
+    int rc = scratch(&work, (size_t)pdas::solve_many_work_doubles(m, k), S(stream));
+    if (rc) return rc;
+    rc = pdas::launch_solve_many(low, m, x, k, work, S(stream));
+    if (work) cudaFreeAsync(work, S(stream));
+    return check_cuda(rc, "cholesky_solve_many");
+}
+
+int pdas_build_v(const double* a, int64_t m, int64_t l0, double dl, double* v, void* stream) {
+    if (m < 1 || l0 < 0) return set_err(PDAS_ERR_ARG, "build_v: bad args");
+    return check_cuda(pdas::launch_build_v(a, m, l0, dl, v, S(stream)), "build_v");
+}
+
+int pdas_sweep_phase1(const double* cols, int64_t m, const double* v, double* inner, int64_t k0,
+                      int64_t k1, void* stream) {
+    if (m < 1 || k0 < 0) return set_err(PDAS_ERR_ARG, "sweep_phase1: bad args");
+    return check_cuda(pdas::launch_sweep_phase1(cols, m, v, inner, k0, k1, S(stream)),
+                      "sweep_phase1");
+}
+
+int pdas_sweep_phase2(double* cols, int64_t m, int64_t l0, const double* inner, double denom,
+                      int64_t k0, int64_t k1, void* stream) {
+    if (m < 1 || k0 <= l0) return set_err(PDAS_ERR_ARG, "sweep_phase2: needs k0 > l0");
+    return check_cuda(pdas::launch_sweep_phase2(cols, m, l0, inner, denom, k0, k1, S(stream)),
+                      "sweep_phase2");
+}
+
+int pdas_solve_sweeps(double* cols, const double* a, const double* d, double* inner, double* v,
+                      int64_t m, int64_t n, int workers, int32_t* fail_dev, void* stream) {
+    (void)inner;
+    (void)v;
+    (void)workers;
+    if (m < 1 || n < 0 || fail_dev == nullptr) return set_err(PDAS_ERR_ARG, "solve_sweeps: bad args");
+    if (m > pdas::cascade_supported_m())
+        return set_err(PDAS_ERR_UNSUPPORTED, "solve_sweeps: m above the compiled configurations");
+    double* denoms = nullptr;
+    int rc = scratch(&denoms, (size_t)(n > 0 ? n : 1), S(stream));
+    if (rc) return rc;
+    rc = pdas::launch_cascade(cols, a, d, m, n, denoms, fail_dev, 0, S(stream));
+    cudaFreeAsync(denoms, S(stream));
+    return check_cuda(rc, "solve_sweeps");
+}
+
+// ------------------------------------------------------------------ iteration
+__global__ void k_iter_reset(PdasIterState* st) {
+    PdasIterState z;
+    memset(&z, 0, sizeof z);
+    z.chol_fail = -1;
+    z.blocking = -1;
+    *st = z;
+}
+
+int pdas_iter_reset(PdasIterState* state, void* stream) {
+    k_iter_reset<<<1, 1, 0, S(stream)>>>(state);
+    return check_cuda(PDAS_OK, "iter_reset");
+}
+
+int pdas_iter_scaling(const double* x, const double* s, int64_t n, double* d,
+                      PdasIterState* state, void* stream) {
+    if (n < 1) return set_err(PDAS_ERR_ARG, "iter_scaling: n < 1");
+    unsigned* flags = &state->interior_flags;
+    return check_cuda(pdas::launch_scaling(x, s, n, d, flags, S(stream)), "iter_scaling");
+}
+
+int pdas_iter_directions(const double* a, int64_t m, int64_t n, const double* dy,
+                         const double* d, const double* x, const double* s, double* dx,
+                         double* ds, double rho, PdasIterState* state, void* stream) {
+    if (m < 1 || n < 1) return set_err(PDAS_ERR_ARG, "iter_directions: bad shape");
+    cudaStream_t st = S(stream);
+    void* parts = nullptr;
+    double* adx = nullptr;
+    double* mvw = nullptr;
+    int rc = scratch((unsigned char**)&parts, (size_t)pdas::directions_partials_bytes(n), st);
+    if (!rc) rc = scratch(&adx, (size_t)m, st);
+    if (!rc) rc = scratch(&mvw, (size_t)pdas::mat_vec_scratch(m, n), st);
+    if (!rc) rc = pdas::launch_directions(a, m, n, dy, d, x, s, dx, ds, parts, st);
+    if (!rc) rc = pdas::launch_mat_vec(a, m, n, dx, adx, mvw, st);
+    if (!rc) rc = pdas::launch_dir_finish(parts, n, adx, m, dy, rho, state, st);
+    if (parts) cudaFreeAsync(parts, st);
+    if (adx) cudaFreeAsync(adx, st);
+    if (mvw) cudaFreeAsync(mvw, st);
+    return check_cuda(rc, "iter_directions");
+}
+
+int pdas_iter_update(double* x, double* y, double* s, const double* dx, const double* dy,
+                     const double* ds, int64_t n, int64_t m, const PdasIterState* state,
+                     void* stream) {
+    if (n < 1 || m < 1 || m > n) return set_err(PDAS_ERR_ARG, "iter_update: bad shape");
+    return check_cuda(pdas::launch_update(x, y, s, dx, dy, ds, n, m, state, S(stream)),
+                      "iter_update");
+}
+
+int pdas_iter_objectives(const double* x, const double* s, const double* c, const double* b,
+                         const double* y, int64_t n, int64_t m, PdasIterState* state,
+                         void* stream) {
+    if (n < 1 || m < 1) return set_err(PDAS_ERR_ARG, "iter_objectives: bad shape");
+    return check_cuda(pdas::launch_dot3(x, s, n, &state->gap, c, x, n, &state->pobj, b, y, m,
+                                        &state->dobj, S(stream)),
+                      "iter_objectives");
+}
+
+int pdas_probe_fp64(double* sink, int64_t iters, int64_t* ops, void* stream) {
+    if (iters < 1 || ops == nullptr) return set_err(PDAS_ERR_ARG, "probe_fp64: bad args");
+    int64_t o = 0;
+    int rc = pdas::launch_fp64_probe(sink, iters, &o, S(stream));
+    *ops = o;
+    return check_cuda(rc, "probe_fp64");
+}
+
+}  // extern "C"

@@ -1,0 +1,73 @@
+// pdas_internal.h -- launcher prototypes and the device-resident iteration
+// state shared by the kernels and the C-ABI layer (abi.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/pdas_b200.h"
+
+namespace pdas {
+
+typedef int64_t idx_t;
+
+constexpr double kCapAlpha = 1e6;  // solver.py:28-29
+
+// k_scaling flag bits (model.py:116-119 with np.min NaN semantics)
+enum : unsigned {
+    IT_X_NAN = 1u,
+    IT_X_LE0 = 2u,
+    IT_S_NAN = 4u,
+    IT_S_LE0 = 8u,
+};
+
+__host__ __device__ inline bool not_interior(unsigned f) {
+    return ((f & IT_X_LE0) && !(f & IT_X_NAN)) || ((f & IT_S_LE0) && !(f & IT_S_NAN));
+}
+
+typedef PdasIterState IterState;
+
+// vec_kernels.cu
+int launch_dot_tree(const double* u, idx_t su, const double* v, idx_t sv, idx_t L, double* out,
+                    cudaStream_t st);
+int launch_mat_t_vec(const double* a, idx_t m, idx_t n, const double* y, double* out,
+                     cudaStream_t st);
+idx_t mat_vec_scratch(idx_t m, idx_t n);
+int launch_mat_vec(const double* a, idx_t m, idx_t n, const double* x, double* out,
+                   double* scratch, cudaStream_t st);
+int launch_scaling(const double* x, const double* s, idx_t n, double* d, unsigned* flags,
+                   cudaStream_t st);
+int launch_directions(const double* a, idx_t m, idx_t n, const double* dy, const double* d,
+                      const double* x, const double* s, double* dx, double* ds, void* partials,
+                      cudaStream_t st);
+idx_t directions_partials_bytes(idx_t n);
+int launch_dir_finish(const void* partials, idx_t n, const double* adx, idx_t m, const double* dy,
+                      double rho, IterState* state, cudaStream_t st);
+int launch_update(double* x, double* y, double* s, const double* dx, const double* dy,
+                  const double* ds, idx_t n, idx_t m, const IterState* state, cudaStream_t st);
+int launch_dot3(const double* u0, const double* v0, idx_t l0, double* o0, const double* u1,
+                const double* v1, idx_t l1, double* o1, const double* u2, const double* v2,
+                idx_t l2, double* o2, cudaStream_t st);
+
+int launch_fp64_probe(double* sink, idx_t iters, idx_t* ops, cudaStream_t st);
+
+// factor_kernels.cu
+int launch_gram(const double* a, idx_t m, idx_t n, const double* d, double* g, cudaStream_t st);
+int launch_cholesky(const double* g, idx_t nn, double eps_rel, double* low, int64_t* fail_dev,
+                    double* work, cudaStream_t st);
+idx_t cholesky_work_doubles(idx_t nn);
+int launch_solve_many(const double* low, idx_t m, double* x, idx_t k, double* work,
+                      cudaStream_t st);
+idx_t solve_many_work_doubles(idx_t m, idx_t k);
+
+// cascade.cu
+int launch_build_v(const double* a, idx_t m, idx_t l0, double dl, double* v, cudaStream_t st);
+int launch_sweep_phase1(const double* cols, idx_t m, const double* v, double* inner, idx_t k0,
+                        idx_t k1, cudaStream_t st);
+int launch_sweep_phase2(double* cols, idx_t m, idx_t l0, const double* inner, double denom,
+                        idx_t k0, idx_t k1, cudaStream_t st);
+int launch_cascade(double* cols, const double* a, const double* d, idx_t m, idx_t n,
+                   double* denoms, int32_t* fail_dev, int block_pivots, cudaStream_t st);
+idx_t cascade_supported_m();
+
+}  // namespace pdas

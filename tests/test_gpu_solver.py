@@ -1,0 +1,193 @@
+"""End-to-end parity of the device-resident solve_lp with the reference:
+same iteration count, same ratio-test selection, and bit-identical trace,
+dy, x, y, s and objective on the seeded LPs (c1 m=50 n=200 seeds 0-4, c2
+m=500 n=5000 seed 0 to convergence, c3 m=2000 n=20000 iteration 1)."""
+
+import numpy as np
+import pytest
+
+from conftest import bits_equal, load_golden, sha
+from oracle import oracle as O
+import spec_cases as SC
+
+pytestmark = pytest.mark.gpu
+
+
+def _trace_rows(tr):
+    return np.array([[r.gap, r.alpha, r.primal_obj, r.dual_obj, r.r_primal, r.r_dual, r.r_comp,
+                      float(r.fallback)] for r in tr])
+
+
+@pytest.mark.parametrize("gap_tol,iters,obj", SC.WORKED_RUNS)
+def test_worked_lp(gpu, gap_tol, iters, obj):
+    P = gpu
+    w = SC.WORKED
+    lp = P.StandardFormLP(P.DenseMatrix.from_array(w["A"]), w["b"], w["c"])
+    p, st, tr = P.solve_lp(lp, P.InteriorPoint(w["x"], w["y"], w["s"]),
+                           P.SolveOptions(gap_tol=gap_tol))
+    assert st is P.Status.OPTIMAL and len(tr) == iters
+    assert tr[0].alpha == SC.WORKED_ALPHA1 or abs(tr[0].alpha - SC.WORKED_ALPHA1) < 1e-15
+    assert P.dot_tree(lp.c, p.x) == obj
+    dirs = P.compute_directions(lp, P.InteriorPoint(w["x"], w["y"], w["s"]),
+                                P.solver.make_backend(lp, "woodbury"))
+    assert abs(dirs.dy[0] - SC.WORKED_DY) < 1e-15
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_c1_trajectory_bitwise(gpu, seed):
+    P = gpu
+    g = load_golden(f"c1_seed{seed}.npz")
+    lp, start = P.gen_random_feasible(50, 200, seed)
+    assert sha(lp.A.data) == str(g["A_sha"])
+    assert bits_equal(lp.b, g["b"]) and bits_equal(lp.c, g["c"])
+    p, st, tr = P.solve_lp(lp, start)
+    assert st.value == str(g["status"])
+    assert len(tr) == len(g["trace"])
+    assert bits_equal(_trace_rows(tr), g["trace"])
+    assert bits_equal(p.x, g["x"]) and bits_equal(p.y, g["y"]) and bits_equal(p.s, g["s"])
+
+
+def test_c1_basis_and_first_iteration(gpu):
+    P = gpu
+    g = load_golden("c1_seed0.npz")
+    lp, start = P.gen_random_feasible(50, 200, 0)
+    basis = P.prepare_woodbury(lp.A)
+    assert bits_equal(basis.L0.as_2d(), g["L0"]) and bits_equal(basis.Y.as_2d(), g["Y"])
+    be = P.solver.make_backend(lp, "woodbury")
+    dirs = P.compute_directions(lp, start, be)
+    assert bits_equal(dirs.dy, g["it1_dy"])
+    assert bits_equal(dirs.dx, g["it1_dx"]) and bits_equal(dirs.ds, g["it1_ds"])
+    assert P.step_length(start, dirs, 0.9) == g["trace"][0][1]
+
+
+def test_blocking_index_sequence(gpu):
+    """Same ratio-test selection (argmin) at every iteration as the reference."""
+    from paper_1502_03543_b200.engine import DeviceProblem, DeviceSolver
+
+    P = gpu
+    g = load_golden("c1_seed0.npz")
+    lp, start = P.gen_random_feasible(50, 200, 0)
+    eng = DeviceSolver(DeviceProblem.from_lp(lp))
+    eng.load_iterate(start.x, start.y, start.s)
+    got = []
+    for _ in range(len(g["blocking"])):
+        got.append(int(eng.iterate().state.blocking))
+    assert got == [int(b) for b in g["blocking"]]
+
+
+def test_c2_to_convergence_bitwise(gpu):
+    from paper_1502_03543_b200.engine import DeviceProblem, DeviceSolver
+
+    P = gpu
+    g = load_golden("c2_seed0.npz")
+    lp, start = P.gen_random_feasible(500, 5000, 0)
+    assert sha(lp.A.data) == str(g["A_sha"])
+    p, st, tr = P.solve_lp(lp, start)
+    assert st.value == str(g["status"]) and len(tr) == len(g["trace"]) == 44
+    assert bits_equal(_trace_rows(tr), g["trace"])
+    assert bits_equal(p.y, g["y"])
+    assert [sha(p.x), sha(p.y), sha(p.s)] == list(g["iter_sha"][-1])
+    # per-iteration iterate hashes and blocking indices through the engine
+    eng = DeviceSolver(DeviceProblem.from_lp(lp))
+    eng.load_iterate(start.x, start.y, start.s)
+    for it in range(3):
+        st_ = eng.iterate().state
+        assert int(st_.blocking) == int(g["blocking"][it])
+        x, y, s = eng.read_iterate()
+        assert [sha(x), sha(y), sha(s)] == list(g["iter_sha"][it])
+
+
+def test_c3_first_iteration_bitwise(gpu):
+    """North-star shape m=2000, n=20000: generator, basis, dy and the new
+    iterate after one PDAS iteration, bit-identical to the reference."""
+    from paper_1502_03543_b200.engine import DeviceProblem, DeviceSolver
+
+    P = gpu
+    g = load_golden("c3_seed0_it1.npz")
+    lp, start = P.gen_random_feasible(2000, 20000, 0)
+    assert sha(lp.A.data) == str(g["A_sha"])
+    assert bits_equal(lp.b, g["b"]) and sha(lp.c) == str(g["c_sha"])
+    prob = DeviceProblem.from_lp(lp)
+    eng = DeviceSolver(prob, L0=prob.validate())
+    from paper_1502_03543_b200 import _device as dv
+
+    assert sha(dv.download(eng.basis.L0)) == str(g["L0_sha"])
+    assert sha(dv.download(eng.basis.Y)) == str(g["Y_sha"])
+    eng.load_iterate(start.x, start.y, start.s)
+    res = eng.iterate()
+    assert bits_equal(dv.download(eng.dy), g["it1_dy"])
+    assert int(res.state.blocking) == int(g["blocking"][0])
+    row = [res.state.gap, res.state.alpha, res.state.pobj, res.state.dobj, res.state.r_primal,
+           res.state.r_dual, res.state.r_comp, 0.0]
+    assert bits_equal(np.array(row), g["trace"][0])
+    x, y, s = eng.read_iterate()
+    assert [sha(x), sha(y), sha(s)] == list(g["iter_sha"][0])
+
+
+def test_direct_backend_matches_oracle(gpu):
+    P = gpu
+    R = O.restated()
+    for seed in (0, 3):
+        lp, start = P.gen_random_feasible(30, 90, seed)
+        p, st, tr = P.solve_lp(lp, start, P.SolveOptions(backend="direct"))
+        a = lp.A.as_2d()
+        xo, yo, so, sto, tro = O.solve_lp(R, a, lp.b, lp.c, start.x, start.y, start.s,
+                                          backend="direct")
+        assert st.value == sto.value and len(tr) == len(tro)
+        assert bits_equal(p.x, xo) and bits_equal(p.y, yo) and bits_equal(p.s, so)
+
+
+def test_gap_contraction_and_direction_identities(gpu):
+    """SPEC.md:499-500 invariants, every iteration."""
+    P = gpu
+    lp, start = P.gen_random_feasible(20, 40, 9)
+    p, st, tr = P.solve_lp(lp, start)
+    assert st is P.Status.OPTIMAL
+    prev = P.duality_gap(start)
+    for r in tr:
+        assert abs(r.gap - (1 - r.alpha) * prev) <= 1e-10 * prev
+        prev = r.gap
+        assert max(r.r_primal, r.r_dual, r.r_comp) <= 1e-8 * (1 + 4.0 * 4.0) * 10
+
+
+def test_error_taxonomy(gpu):
+    P = gpu
+    lp, start = P.gen_random_feasible(5, 9, 1)
+    bad = start.copy()
+    bad.x[0] = -1.0
+    with pytest.raises(P.NotInterior):
+        P.solve_lp(lp, bad)
+    bad = start.copy()
+    bad.y[0] += 1.0
+    with pytest.raises(P.NotFeasible):
+        P.solve_lp(lp, bad)
+    a = lp.A.as_2d().copy()
+    a[1] = a[0]
+    lp2 = P.StandardFormLP(P.DenseMatrix.from_array(a), lp.b, lp.c)
+    with pytest.raises(P.RankDeficient):
+        P.solve_lp(lp2, start)
+    a = lp.A.as_2d().copy()
+    a[0, 0] = np.nan
+    with pytest.raises(P.NonFiniteEntry):
+        P.solve_lp(P.StandardFormLP(P.DenseMatrix.from_array(a), lp.b, lp.c), start)
+    with pytest.raises(P.NotPositiveDefinite):
+        P.cholesky_factor(P.DenseMatrix.from_rows([[1, 2], [2, 1]]))
+    with pytest.raises(P.SingularUpdate):
+        P.solve_woodbury(P.prepare_woodbury(P.DenseMatrix.from_rows([[1.0]])),
+                         P.DenseMatrix.from_rows([[1.0]]), [1e-14], [1.0])
+
+
+def test_iter_limit_and_trace_writers(gpu):
+    P = gpu
+    lp, start = P.gen_random_feasible(10, 30, 4)
+    p, st, tr = P.solve_lp(lp, start, P.SolveOptions(max_iter=3))
+    assert st is P.Status.ITER_LIMIT and len(tr) == 3
+    csv = P.solver.trace_to_csv(tr)
+    assert csv.splitlines()[0] == P.solver.TRACE_CSV_HEADER and len(csv.splitlines()) == 4
+    assert len(__import__("json").loads(P.solver.trace_to_json(tr))) == 3
+
+
+def test_z_inverse_check_hand_case(gpu):
+    P = gpu
+    r = P.z_inverse_check(P.DenseMatrix.from_rows([[2.0]]), [3.0])
+    assert r < 1e-15
