@@ -110,6 +110,21 @@ int pdas_sweep_phase2(double* cols, int64_t m, int64_t l0, const double* inner, 
 int pdas_solve_sweeps(double* cols, const double* a, const double* d, double* inner, double* v,
                       int64_t m, int64_t n, int workers, int32_t* fail_dev, void* stream);
 
+/* Same cascade with a caller-owned workspace (no per-call allocation): ws
+ * holds the step denominators and the inter-CTA panel flags; it must be
+ * zeroed once, then reused with epoch = 1, 2, 3, ... (strictly increasing on
+ * that ws).  Used by the solver engine once per PDAS iteration. */
+int64_t pdas_cascade_ws_bytes(int64_t m, int64_t n);
+int pdas_solve_sweeps_ws(double* cols, const double* a, const double* d, int64_t m, int64_t n,
+                         void* ws, int32_t epoch, int32_t* fail_dev, void* stream);
+
+/* cholesky_solve (linalg.py:126-132) for ONE right-hand side, in place on
+ * x (m): the per-iteration x0 = L0^-T L0^-1 (A x) of init_workspace
+ * (normal.py:123).  Same rounding sequence as cholesky_solve_many with k=1,
+ * scheduled for latency (one CTA: right-looking forward sweep, backward
+ * chain fed by helper warps). */
+int pdas_cholesky_solve_one(const double* low, int64_t m, double* x, void* stream);
+
 /* ---- fused per-iteration path (adascale/solver.py) ------------------------- */
 
 /* Reset *state (all zero, chol_fail = -1). */

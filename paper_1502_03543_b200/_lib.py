@@ -70,6 +70,9 @@ SIGNATURES = {
     "pdas_sweep_phase1": (ctypes.c_int, [_VP, _I64, _VP, _VP, _I64, _I64, _VP]),
     "pdas_sweep_phase2": (ctypes.c_int, [_VP, _I64, _I64, _VP, _D, _I64, _I64, _VP]),
     "pdas_solve_sweeps": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _I64, _I64, ctypes.c_int, _VP, _VP]),
+    "pdas_cascade_ws_bytes": (ctypes.c_int64, [_I64, _I64]),
+    "pdas_solve_sweeps_ws": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, _VP, ctypes.c_int32, _VP, _VP]),
+    "pdas_cholesky_solve_one": (ctypes.c_int, [_VP, _I64, _VP, _VP]),
     "pdas_iter_reset": (ctypes.c_int, [_VP, _VP]),
     "pdas_iter_scaling": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
     "pdas_iter_directions": (ctypes.c_int, [_VP, _I64, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _D, _VP, _VP]),

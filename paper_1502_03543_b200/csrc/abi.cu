@@ -147,12 +147,43 @@ int pdas_solve_sweeps(double* cols, const double* a, const double* d, double* in
     if (m < 1 || n < 0 || fail_dev == nullptr) return set_err(PDAS_ERR_ARG, "solve_sweeps: bad args");
     if (m > pdas::cascade_supported_m())
         return set_err(PDAS_ERR_UNSUPPORTED, "solve_sweeps: m above the compiled configurations");
-    double* denoms = nullptr;
-    int rc = scratch(&denoms, (size_t)(n > 0 ? n : 1), S(stream));
+    unsigned char* ws = nullptr;
+    const size_t bytes = (size_t)pdas_cascade_ws_bytes(m, n);
+    int rc = scratch(&ws, bytes, S(stream));
     if (rc) return rc;
-    rc = pdas::launch_cascade(cols, a, d, m, n, denoms, fail_dev, 0, S(stream));
-    cudaFreeAsync(denoms, S(stream));
-    return check_cuda(rc, "solve_sweeps");
+    cudaMemsetAsync(ws, 0, bytes, S(stream));
+    rc = pdas_solve_sweeps_ws(cols, a, d, m, n, ws, 1, fail_dev, stream);
+    cudaFreeAsync(ws, S(stream));
+    return rc;
+}
+
+int64_t pdas_cascade_ws_bytes(int64_t m, int64_t n) {
+    const int64_t nd = n > 0 ? n : 1;
+    return (int64_t)(((nd * 8 + 255) / 256) * 256 + pdas::cascade_flags_count(m, n) * 4);
+}
+
+int pdas_solve_sweeps_ws(double* cols, const double* a, const double* d, int64_t m, int64_t n,
+                         void* ws, int32_t epoch, int32_t* fail_dev, void* stream) {
+    if (m < 1 || n < 0 || fail_dev == nullptr || ws == nullptr || epoch < 1)
+        return set_err(PDAS_ERR_ARG, "solve_sweeps_ws: bad args");
+    if (m > pdas::cascade_supported_m())
+        return set_err(PDAS_ERR_UNSUPPORTED, "solve_sweeps: m above the compiled configurations");
+    const int64_t nd = n > 0 ? n : 1;
+    double* denoms = static_cast<double*>(ws);
+    int* flags = reinterpret_cast<int*>(static_cast<unsigned char*>(ws) + ((nd * 8 + 255) / 256) * 256);
+    return check_cuda(
+        pdas::launch_cascade(cols, a, d, m, n, denoms, fail_dev, flags, epoch, 0, S(stream)),
+        "solve_sweeps");
+}
+
+int pdas_cholesky_solve_one(const double* low, int64_t m, double* x, void* stream) {
+    if (m < 1) return set_err(PDAS_ERR_ARG, "cholesky_solve_one: bad shape");
+    double* work = nullptr;
+    int rc = scratch(&work, (size_t)pdas::solve_one_work_doubles(m), S(stream));
+    if (rc) return rc;
+    rc = pdas::launch_solve_one(low, m, x, work, S(stream));
+    if (work) cudaFreeAsync(work, S(stream));
+    return check_cuda(rc, "cholesky_solve_one");
 }
 
 // ------------------------------------------------------------------ iteration

@@ -315,6 +315,8 @@ int launch_solve_many(const double* low, idx_t m, double* x, idx_t k, double* wo
                       cudaStream_t st) {
     if (m < 1 || k < 0) return PDAS_ERR_ARG;
     if (k == 0) return PDAS_OK;
+    if (k == 1 && 3 * m * (idx_t)sizeof(double) <= 200 * 1024)
+        return launch_solve_one(low, m, x, work, st);
     size_t smem = (size_t)4 * m * sizeof(double);
     if (smem > 200 * 1024) return PDAS_ERR_UNSUPPORTED;
     if (smem > 48 * 1024)

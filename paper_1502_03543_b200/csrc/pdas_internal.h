@@ -67,7 +67,13 @@ int launch_sweep_phase1(const double* cols, idx_t m, const double* v, double* in
 int launch_sweep_phase2(double* cols, idx_t m, idx_t l0, const double* inner, double denom,
                         idx_t k0, idx_t k1, cudaStream_t st);
 int launch_cascade(double* cols, const double* a, const double* d, idx_t m, idx_t n,
-                   double* denoms, int32_t* fail_dev, int block_pivots, cudaStream_t st);
+                   double* denoms, int32_t* fail_dev, int* flags, int epoch, int block_pivots,
+                   cudaStream_t st);
 idx_t cascade_supported_m();
+idx_t cascade_flags_count(idx_t m, idx_t n);
+
+// solve_kernels.cu (single right-hand side, latency-optimised)
+int launch_solve_one(const double* low, idx_t m, double* x, double* work, cudaStream_t st);
+idx_t solve_one_work_doubles(idx_t m);
 
 }  // namespace pdas

@@ -167,6 +167,11 @@ class DeviceSolver:
         if backend == "woodbury":
             self.basis = basis or prepare_basis(prob, L0)
             self.cols = dv.empty(m * (n + 1))
+            from ._lib import load
+
+            self.casc_ws = t.zeros(int(load().pdas_cascade_ws_bytes(m, n)), dtype=t.uint8,
+                                   device=dv.device())
+            self.epoch = 0
             self.xcol = self.cols[m * n:]
         self.x = dv.empty(n)
         self.y = dv.empty(m)
@@ -245,10 +250,11 @@ class DeviceSolver:
             self.cols[:m * n].copy_(B.Y, non_blocking=True)  # init_workspace (normal.py:121-123)
             self.xcol.copy_(self.rhs, non_blocking=True)
             d_solve_many(B.L0, m, self.xcol, 1)
-            call("pdas_solve_sweeps", dv.ptr(self.cols), dv.ptr(P.A), dv.ptr(self.d), None, None,
-                 m, n, 1, self._sptr(OFF_CASCADE_FAIL), st)
+            self.epoch += 1
+            call("pdas_solve_sweeps_ws", dv.ptr(self.cols), dv.ptr(P.A), dv.ptr(self.d), m, n,
+                 dv.ptr(self.casc_ws), self.epoch, self._sptr(OFF_CASCADE_FAIL), st)
             self.dy = self.xcol
-            self.launches += 3 + 2 * ((n + 63) // 64)
+            self.launches += 2 + 2 * ((n + 63) // 64)
         else:
             self._solve_direct_into(self.dy_direct, self._sptr(OFF_CHOL_FAIL))
             self.dy = self.dy_direct
