@@ -30,12 +30,19 @@
 //   traffic is 16/CT B; the fp64 pipe (4 separately rounded ops per
 //   element-step) becomes the bound.
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "pdas_internal.h"
 #include "tma.cuh"
 
 namespace pdas {
+
+// Diagnostic ablation switch (PDAS_CASCADE_MODE): 0 = normal; 1 = skip the
+// cross-thread reduction; 2 = skip the per-thread partials.  Results are
+// wrong for modes != 0; used only by tools/cascade_time.py experiments.
+__device__ int g_casc_mode = 0;
+__device__ long long g_casc_trace[2 * 16 * 6];
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -134,27 +141,44 @@ struct Tile {
 
     // v = A[:,l] * f for this thread's rows, from a column base pointer
     // (shared-memory stage or global).  Absent rows get exactly +0.0.
-    template <bool GLOBAL>
+    // FULL (warp-uniform): every row this thread owns exists -- no selects.
+    __device__ __forceinline__ bool full() const {
+        return !GEN && hv == (R >= 32 ? 0xffffffffu : (1u << (R & 31)) - 1u);
+    }
+
+    template <bool GLOBAL, bool FULL>
     __device__ __forceinline__ void make_v(const double* ac, double f, double (&vl)[R],
                                            double (&vh)[R]) const {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            double al = 0.0, ah = 0.0;
-            if (vlo(r)) al = GLOBAL ? __ldcg(ac + row(r)) : ac[row(r)];
-            if (vhi(r)) ah = GLOBAL ? __ldcg(ac + row(r) + H) : ac[row(r) + H];
-            vl[r] = vlo(r) ? al * f : 0.0;
-            vh[r] = vhi(r) ? ah * f : 0.0;
+            if (FULL) {
+                const double al = GLOBAL ? __ldcg(ac + row(r)) : ac[row(r)];
+                const double ah = GLOBAL ? __ldcg(ac + row(r) + H) : ac[row(r) + H];
+                vl[r] = al * f;
+                vh[r] = ah * f;
+            } else {
+                double al = 0.0, ah = 0.0;
+                if (vlo(r)) al = GLOBAL ? __ldcg(ac + row(r)) : ac[row(r)];
+                if (vhi(r)) ah = GLOBAL ? __ldcg(ac + row(r) + H) : ac[row(r) + H];
+                vl[r] = vlo(r) ? al * f : 0.0;
+                vh[r] = vhi(r) ? ah * f : 0.0;
+            }
         }
     }
 
-    template <bool GLOBAL>
+    template <bool GLOBAL, bool FULL>
     __device__ __forceinline__ void load_p(const double* pc, double (&pl)[R], double (&ph)[R]) const {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            pl[r] = 0.0;
-            ph[r] = 0.0;
-            if (vlo(r)) pl[r] = GLOBAL ? __ldcg(pc + row(r)) : pc[row(r)];
-            if (vhi(r)) ph[r] = GLOBAL ? __ldcg(pc + row(r) + H) : pc[row(r) + H];
+            if (FULL) {
+                pl[r] = GLOBAL ? __ldcg(pc + row(r)) : pc[row(r)];
+                ph[r] = GLOBAL ? __ldcg(pc + row(r) + H) : pc[row(r) + H];
+            } else {
+                pl[r] = 0.0;
+                ph[r] = 0.0;
+                if (vlo(r)) pl[r] = GLOBAL ? __ldcg(pc + row(r)) : pc[row(r)];
+                if (vhi(r)) ph[r] = GLOBAL ? __ldcg(pc + row(r) + H) : pc[row(r) + H];
+            }
         }
     }
 
@@ -220,18 +244,24 @@ struct Tile {
         }
     }
 
+    // x -= g*P.  Absent rows are never touched (they stay exactly +0.0 even
+    // when g is not finite), so the !FULL path predicates them off.
+    template <bool FULL>
     __device__ __forceinline__ void axpy(const double (&g)[C], const double (&pl)[R],
                                          const double (&ph)[R]) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const bool lo = vlo(r), hi = vhi(r);
+            const bool lo = FULL || vlo(r), hi = FULL || vhi(r);
+            if (lo) {
 #pragma unroll
-            for (int c = 0; c < C; ++c) {
-                if (lo) {
+                for (int c = 0; c < C; ++c) {
                     double q0 = g[c] * pl[r];
                     xl[r][c] = xl[r][c] - q0;
                 }
-                if (hi) {
+            }
+            if (hi) {
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
                     double q1 = g[c] * ph[r];
                     xh[r][c] = xh[r][c] - q1;
                 }
@@ -243,34 +273,68 @@ struct Tile {
 // ------------------------------------------------------------ TMA pipeline
 // Stage s = [P_l | A[:,l]] (2 x mp doubles).  full[s]: producer arrive +
 // TMA bytes.  empty[s]: one arrival per consumer group once it is done.
-// `k` counts stage uses (identical in every thread of the CTA).
+// `k` counts stage uses (identical in every thread of the CTA).  S (stage
+// count) is a compile-time constant so stage arithmetic is shifts/masks.
+constexpr int kMaxBlock = 128;  // pivots per block (B) upper bound
+
+template <int S>
 struct Pipe {
     double* buf;
     uint64_t* full;
     uint64_t* empty;
-    int S, mp;
+    uint32_t full_a, empty_a, buf_a;  // shared-window addresses (no cvta in the loop)
+    int mp;
     unsigned k;
+    double* sd;    // d[l - base] for the kernel's pivot window (shared memory)
+    double* sden;  // denom[l - base]
 };
 
-__device__ __forceinline__ void pipe_issue(Pipe& p, unsigned use, const double* pcol,
-                                           const double* acol, int m) {
-    const int s = (int)(use % p.S);
-    if (use >= (unsigned)p.S) mbar_wait(p.empty + s, ((use / p.S) - 1u) & 1u);
-    const uint32_t bytes = (uint32_t)m * (uint32_t)sizeof(double);
-    double* dst = p.buf + (size_t)s * 2 * p.mp;
-    if (pcol) {
-        mbar_arrive_expect_tx(p.full + s, 2 * bytes);
-        tma_load_1d(dst, pcol, bytes, p.full + s);
-    } else {
-        mbar_arrive_expect_tx(p.full + s, bytes);
-    }
-    tma_load_1d(dst + p.mp, acol, bytes, p.full + s);
+__device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITA_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAITA_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
 }
 
-// dynamic smem: red[G][C*T] | bc[G][C] | full[S] | empty[S] | stages
+__device__ __forceinline__ void mbar_arrive_a(uint32_t a) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+
+template <int S>
+__device__ __forceinline__ void pipe_issue(Pipe<S>& p, unsigned use, const double* pcol,
+                                           const double* acol, int m, bool wait_empty = true) {
+    const uint32_t s = use % S;
+    const uint32_t fb = p.full_a + 8 * s;
+    if (wait_empty && use >= (unsigned)S) mbar_wait_a(p.empty_a + 8 * s, ((use / S) - 1u) & 1u);
+    const uint32_t bytes = (uint32_t)m * (uint32_t)sizeof(double);
+    const uint32_t dst = p.buf_a + s * 2u * (uint32_t)p.mp * 8u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
+                 "r"(pcol ? 2 * bytes : bytes)
+                 : "memory");
+    if (pcol)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+            "[%3];" ::"r"(dst),
+            "l"(pcol), "r"(bytes), "r"(fb)
+            : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+        "[%3];" ::"r"(dst + (uint32_t)p.mp * 8u),
+        "l"(acol), "r"(bytes), "r"(fb)
+        : "memory");
+}
+
+// dynamic smem: red[G][C*T] | bc[G][C] | sd[2*kMaxBlock] | sden[2*kMaxBlock]
+//               | full[S] | empty[S] | stages
 template <int T, int C, int G>
 __host__ __device__ constexpr size_t casc_head_bytes(int S) {
-    return (((size_t)G * C * T + (size_t)G * C + 2 * (size_t)S) * sizeof(double) + 127) & ~(size_t)127;
+    return (((size_t)G * C * T + (size_t)G * C + 4 * kMaxBlock + 2 * (size_t)S) * sizeof(double) +
+            127) & ~(size_t)127;
 }
 
 template <int T, int C, int G>
@@ -279,155 +343,629 @@ __host__ __device__ inline size_t casc_smem_bytes(int S, int m) {
     return casc_head_bytes<T, C, G>(S) + (size_t)S * 2 * mp * sizeof(double);
 }
 
-template <int T, int C, int G>
-__device__ __forceinline__ void carve(double*& red, double*& bc, Pipe& pp, int S, int m) {
+template <int T, int C, int G, int S>
+__device__ __forceinline__ void carve(double*& red, double*& bc, Pipe<S>& pp, bool tma, int m) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     red = reinterpret_cast<double*>(smem_raw);
     bc = red + G * C * T;
-    pp.full = reinterpret_cast<uint64_t*>(bc + G * C);
-    pp.empty = pp.full + (S > 0 ? S : 0);
-    pp.buf = reinterpret_cast<double*>(smem_raw + casc_head_bytes<T, C, G>(S > 0 ? S : 0));
-    pp.S = S > 0 ? S : 1;
+    pp.sd = bc + G * C;
+    pp.sden = pp.sd + 2 * kMaxBlock;
+    pp.full = reinterpret_cast<uint64_t*>(pp.sden + 2 * kMaxBlock);
+    pp.empty = pp.full + S;
+    pp.buf = reinterpret_cast<double*>(smem_raw + casc_head_bytes<T, C, G>(S));
+    pp.full_a = smem_addr(pp.full);
+    pp.empty_a = smem_addr(pp.empty);
+    pp.buf_a = smem_addr(pp.buf);
     pp.mp = (m + 1) & ~1;
     pp.k = 0;
-    if (S > 0) {
-        if (threadIdx.x == 0) {
-            for (int s = 0; s < S; ++s) {
-                mbar_init(pp.full + s, 1);
-                mbar_init(pp.empty + s, G);
-            }
-            mbar_fence_init();
+    if (tma && threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(pp.full + s, 1);
+            mbar_init(pp.empty + s, G);
         }
-        __syncthreads();
+        mbar_fence_init();
+    }
+}
+
+// Stage the pivot scalars of [lo, hi) (relative to `base`) into shared memory.
+template <int S>
+__device__ __forceinline__ void stage_scalars(Pipe<S>& pp, const double* __restrict__ d,
+                                              const double* __restrict__ denoms, idx_t base,
+                                              idx_t lo, idx_t hi, bool with_d) {
+    for (idx_t l = lo + threadIdx.x; l < hi; l += blockDim.x) {
+        if (with_d) pp.sd[l - base] = __ldg(d + l);
+        pp.sden[l - base] = __ldcg(denoms + l);
     }
 }
 
 // Apply pivots [l0, l1) whose final columns live in global memory to the
-// register tile, in ascending order.  `producer` is the CTA's thread 0.
-template <bool TMA, int T, int R, int C, bool GEN>
-__device__ __forceinline__ void apply_global(Tile<T, R, C, GEN>& tl, Pipe& pp,
-                                             const double* __restrict__ cols,
-                                             const double* __restrict__ a,
-                                             const double* __restrict__ d,
-                                             const double* __restrict__ denoms, idx_t l0,
-                                             idx_t l1, bool producer) {
-    const int cnt = (int)(l1 - l0);
-    if (cnt <= 0) return;
+// register tile, in ascending order.  d and denom come from the shared
+// window (index l - base).  `producer` is the CTA's thread 0.
+template <bool TMA, bool FULL, int S, int T, int R, int C, bool GEN>
+__device__ __forceinline__ void apply_impl(Tile<T, R, C, GEN>& tl, Pipe<S>& pp,
+                                           const double* __restrict__ cols,
+                                           const double* __restrict__ a, idx_t base, idx_t l0,
+                                           int cnt, bool producer) {
     const int m = tl.m;
     const unsigned k0 = pp.k;
-    if (TMA && producer) {
-        const int pre = cnt < pp.S ? cnt : pp.S;
-        for (int i = 0; i < pre; ++i)
-            pipe_issue(pp, k0 + i, cols + (l0 + i) * m, a + (l0 + i) * m, m);
-    }
+    const double* sd = pp.sd + (l0 - base);
+    const double* sden = pp.sden + (l0 - base);
+    const double* ga = a + l0 * m;      // global A column of pivot l0 + j: ga + j*m
+    const double* gc = cols + l0 * m;   // global P column
+    const int stage = 2 * pp.mp;
+    const bool trace = g_casc_mode == 3 && blockIdx.x == 0 && l0 == 1280 &&
+                       (threadIdx.x == 0 || threadIdx.x == blockDim.x - 32);
+    const int tslot = threadIdx.x == 0 ? 0 : 1;
+#define PDAS_TRACE(pt)                                                              \
+    if (trace && j >= 8 && j < 24) g_casc_trace[((tslot * 16 + (j - 8)) * 6) + (pt)] = clock64();
     for (int j = 0; j < cnt; ++j) {
-        const idx_t l = l0 + j;
         const unsigned use = k0 + j;
-        const int s = (int)(use % pp.S);
         const double* pc;
         const double* ac;
+        PDAS_TRACE(0)
         if (TMA) {
-            mbar_wait(pp.full + s, (use / pp.S) & 1u);
-            pc = pp.buf + (size_t)s * 2 * pp.mp;
+            const uint32_t s = use % S;
+            mbar_wait_a(pp.full_a + 8 * s, (use / S) & 1u);
+            pc = pp.buf + s * stage;
             ac = pc + pp.mp;
         } else {
-            pc = cols + l * m;
-            ac = a + l * m;
+            pc = gc + (size_t)j * m;
+            ac = ga + (size_t)j * m;
         }
-        const double dl = __ldg(d + l);
+        PDAS_TRACE(1)
+        const double dl = sd[j];
         const bool active = dl != 1.0;
         double part[C];
         if (active) {
             double vl[R], vh[R];
-            tl.template make_v<!TMA>(ac, dl - 1.0, vl, vh);
+            tl.template make_v<!TMA, FULL>(ac, dl - 1.0, vl, vh);
             tl.partials(vl, vh, part);
             tl.publish(part);
         }
+        PDAS_TRACE(2)
         tl.sync();  // B1: partials published; stage of use-1 fully consumed
         if (TMA && j > 0) {
-            if (tl.t == 0) mbar_arrive(pp.empty + (int)((use - 1) % pp.S));
-            if (producer && j - 1 + pp.S < cnt)
-                pipe_issue(pp, use - 1 + pp.S, cols + (l - 1 + pp.S) * m, a + (l - 1 + pp.S) * m,
-                           m);
+            if (tl.t == 0) mbar_arrive_a(pp.empty_a + 8 * ((use - 1) % S));
+            if (producer && j - 1 + S < cnt)
+                pipe_issue(pp, use - 1 + S, gc + (size_t)(j - 1 + S) * m,
+                           ga + (size_t)(j - 1 + S) * m, m);
         }
+        PDAS_TRACE(3)
         if (active) {
-            const double denom = __ldcg(denoms + l);
             double g[C];
-            tl.template finish<true>(part, denom, g);
+            tl.template finish<true>(part, sden[j], g);
+            PDAS_TRACE(4)
             double pl[R], ph[R];
-            tl.template load_p<!TMA>(pc, pl, ph);
-            tl.axpy(g, pl, ph);
+            tl.template load_p<!TMA, FULL>(pc, pl, ph);
+            tl.template axpy<FULL>(g, pl, ph);
         }
+        PDAS_TRACE(5)
     }
+#undef PDAS_TRACE
     if (TMA) {
         tl.sync();
-        if (tl.t == 0) mbar_arrive(pp.empty + (int)((k0 + cnt - 1) % pp.S));
+        if (tl.t == 0) mbar_arrive_a(pp.empty_a + 8 * ((k0 + cnt - 1) % S));
         pp.k = k0 + cnt;
     }
+}
+
+__device__ __forceinline__ void named_arrive(int id, int nthreads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Ping-pong schedule for two column groups sharing one pivot pipeline.
+// Each group iterates  [compute: axpy(l-1) + partials(l)] -> B1 -> reduce(l)
+// -> B2, and the compute phases of the two groups are ordered by a token
+// (named barriers 3/4, 2T threads: the finishing group arrives, the next
+// one syncs), so one group's serial reduction (shared-memory hop, shuffles,
+// the fp64 division) always runs while the other group keeps the fp64 pipe
+// busy.  Stages are recycled two pivots behind so the producer (CTA thread
+// 0, group 0) never waits on the other group's current compute phase.
+template <int S, bool FULL, int T, int R, int C>
+__device__ __forceinline__ void apply_pingpong(Tile<T, R, C, false>& tl, Pipe<S>& pp, int grp,
+                                               const double* __restrict__ cols,
+                                               const double* __restrict__ a, idx_t l0, int cnt,
+                                               bool producer) {
+    static_assert(S >= 4, "ping-pong recycles stages three pivots behind");
+    const int m = tl.m;
+    const int tok_mine = 3 + grp, tok_other = 4 - grp;
+    const double* ga = a + l0 * m;
+    const double* gc = cols + l0 * m;
+    const int stage = 2 * pp.mp;
+    const double* sd = pp.sd;  // window base == l0 in the update kernel
+    const double* sden = pp.sden;
+    if (grp == 1) named_arrive(3, 2 * T);  // group 0 computes first
+    double g[C];
+    bool prev_active = false;
+    const double* prev_pc = nullptr;
+    for (int j = 0; j <= cnt; ++j) {
+        // ---- compute phase, token-ordered between the groups
+        named_bar(tok_mine, 2 * T);
+        if (prev_active) {
+            double pl[R], ph[R];
+            tl.template load_p<false, FULL>(prev_pc, pl, ph);
+            tl.template axpy<FULL>(g, pl, ph);
+        }
+        bool active = false;
+        double part[C];
+        const double* pc = nullptr;
+        if (j < cnt) {
+            const unsigned use = pp.k + j;
+            const uint32_t s = use % S;
+            mbar_wait_a(pp.full_a + 8 * s, (use / S) & 1u);
+            pc = pp.buf + s * stage;
+            const double dl = sd[j];
+            active = dl != 1.0;
+            if (active) {
+                double vl[R], vh[R];
+                tl.template make_v<false, FULL>(pc + pp.mp, dl - 1.0, vl, vh);
+                tl.partials(vl, vh, part);
+                tl.publish(part);
+            }
+        }
+        named_arrive(tok_other, 2 * T);
+        if (j == cnt) break;
+        // ---- reduce phase
+        tl.sync();  // B1: partials published; stage of use j-1 consumed by this group
+        if (j >= 2) {
+            const unsigned done = pp.k + j - 2;  // released two pivots behind
+            if (tl.t == 0) mbar_arrive_a(pp.empty_a + 8 * (done % S));
+        }
+        // refill three behind: the other group released that use an iteration ago
+        if (producer && j >= 3 && j - 3 + S < cnt)
+            pipe_issue(pp, pp.k + j - 3 + S, gc + (size_t)(j - 3 + S) * m,
+                       ga + (size_t)(j - 3 + S) * m, m);
+        if (active) tl.template finish<true>(part, sden[j], g);
+        prev_active = active;
+        prev_pc = pc;
+    }
+    if (grp == 0) named_bar(3, 2 * T);  // consume group 1's last token
+    // release the last two uses (j = cnt-2, cnt-1) once this group is done
+    tl.sync();
+    if (tl.t == 0) {
+        for (int j = cnt - 2 > 0 ? cnt - 2 : 0; j < cnt; ++j)
+            mbar_arrive_a(pp.empty_a + 8 * ((pp.k + j) % S));
+    }
+    pp.k += cnt;
+}
+
+// ------------------------------------------------------------ split schedule
+// Half-tile skew (the update kernel's main path).  The tile's C columns are
+// two halves A = [0, C/2) and B = [C/2, C) processed half a pivot apart, so
+// each phase carries the fp64 work of one half while the reducer warps of the
+// other half run their serial chain (shared-memory hop, shuffles, division):
+//   P(j): axpy B(j-1), partials B(j), reduce A(j) [warps of half A] | barrier
+//   Q(j): axpy A(j),   partials A(j+1), reduce B(j) [warps of half B] | barrier
+// Every column still sees its pivots in ascending order with the reference
+// rounding sequence; only the interleaving of independent columns changes.
+template <int H0, int NH, int T, int R, int C>
+__device__ __forceinline__ void half_partials(const Tile<T, R, C, false>& tl, const double (&vl)[R],
+                                              const double (&vh)[R], double* red) {
+#pragma unroll
+    for (int c = 0; c < NH; ++c) {
+        double s[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            double lo = vl[r] * tl.xl[r][H0 + c];
+            double hi = vh[r] * tl.xh[r][H0 + c];
+            s[r] = lo + hi;
+        }
+        red[c * T + tl.t] = lane_tree<R>(s);
+    }
+}
+
+template <bool FULL, int H0, int NH, int T, int R, int C>
+__device__ __forceinline__ void half_axpy(Tile<T, R, C, false>& tl, const double* bc,
+                                          const double* pc) {
+    double g[NH];
+#pragma unroll
+    for (int c = 0; c < NH; ++c) g[c] = bc[c];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const bool hi = FULL || tl.vhi(r);
+        const double pl = pc[tl.row(r)];
+        const double ph = hi ? pc[tl.row(r) + tl.H] : 0.0;
+#pragma unroll
+        for (int c = 0; c < NH; ++c) {
+            double q0 = g[c] * pl;
+            tl.xl[r][H0 + c] = tl.xl[r][H0 + c] - q0;
+        }
+        if (hi) {
+#pragma unroll
+            for (int c = 0; c < NH; ++c) {
+                double q1 = g[c] * ph;
+                tl.xh[r][H0 + c] = tl.xh[r][H0 + c] - q1;
+            }
+        }
+    }
+}
+
+// Reducer warp for column c of a half: levels T/2 .. 1 then g = inner/denom.
+template <int T>
+__device__ __forceinline__ void half_reduce(const double* red, int c, int lane, double denom,
+                                            double* bc) {
+    constexpr int NW = T / 32;
+    double q[NW];
+#pragma unroll
+    for (int k = 0; k < NW; ++k) q[k] = red[c * T + lane + 32 * k];
+    const double v = warp_butterfly32(lane_tree<NW>(q));
+    if (lane == 0) bc[c] = v / denom;
+}
+
+template <int S, bool FULL, int T, int R, int C>
+__device__ __forceinline__ void apply_split(Tile<T, R, C, false>& tl, Pipe<S>& pp,
+                                            const double* __restrict__ cols,
+                                            const double* __restrict__ a, idx_t l0, int cnt,
+                                            bool producer) {
+    static_assert(C % 2 == 0 && C / 2 <= T / 32, "one reducer warp per half column");
+    constexpr int HC = C / 2;
+    const int m = tl.m;
+    const int warp = tl.t >> 5, lane = tl.t & 31;
+    double* redA = tl.red;
+    double* redB = tl.red + HC * T;
+    double* bcA = tl.bc;
+    double* bcB = tl.bc + HC;
+    const double* sd = pp.sd;  // window base == l0
+    const double* sden = pp.sden;
+    const double* ga = a + l0 * m;
+    const double* gc = cols + l0 * m;
+    const int stage = 2 * pp.mp;
+    const unsigned k0 = pp.k;
+    const bool trace = g_casc_mode == 3 && blockIdx.x == 0 && l0 == 1280 &&
+                       (threadIdx.x == 0 || threadIdx.x == blockDim.x - 32);
+    const int tslot = threadIdx.x == 0 ? 0 : 1;
+#define PDAS_TRACE(pt)                                                              \
+    if (trace && j >= 8 && j < 24) g_casc_trace[((tslot * 16 + (j - 8)) * 6) + (pt)] = clock64();
+    auto sptr = [&](int j) -> const double* { return pp.buf + ((k0 + j) % S) * stage; };
+    auto swait = [&](int j) { mbar_wait_a(pp.full_a + 8 * ((k0 + j) % S), ((k0 + j) / S) & 1u); };
+    auto act = [&](int j) { return sd[j] != 1.0; };
+    // Q(-1): partials A(0)
+    swait(0);
+    if (act(0)) {
+        double vl[R], vh[R];
+        tl.template make_v<false, FULL>(sptr(0) + pp.mp, sd[0] - 1.0, vl, vh);
+        half_partials<0, HC>(tl, vl, vh, redA);
+    }
+    tl.sync();
+    for (int j = 0; j < cnt; ++j) {
+        const bool aj = act(j);
+        PDAS_TRACE(0)
+        // ---- P(j)
+        if (j > 0 && act(j - 1)) half_axpy<FULL, HC, HC>(tl, bcB, sptr(j - 1));
+        if (aj) {
+            double vl[R], vh[R];
+            tl.template make_v<false, FULL>(sptr(j) + pp.mp, sd[j] - 1.0, vl, vh);
+            half_partials<HC, HC>(tl, vl, vh, redB);
+            if (warp < HC) half_reduce<T>(redA, warp, lane, sden[j], bcA);
+        }
+        PDAS_TRACE(1)
+        tl.sync();
+        PDAS_TRACE(2)
+        // stage j-1 had its last reader (axpy B) in P(j): recycle it
+        if (j > 0) {
+            if (tl.t == 0) mbar_arrive_a(pp.empty_a + 8 * ((k0 + j - 1) % S));
+            if (producer && j - 1 + S < cnt)
+                pipe_issue(pp, k0 + j - 1 + S, gc + (size_t)(j - 1 + S) * m,
+                           ga + (size_t)(j - 1 + S) * m, m);
+        }
+        // ---- Q(j)
+        if (aj) half_axpy<FULL, 0, HC>(tl, bcA, sptr(j));
+        if (j + 1 < cnt) {
+            swait(j + 1);
+            if (act(j + 1)) {
+                double vl[R], vh[R];
+                tl.template make_v<false, FULL>(sptr(j + 1) + pp.mp, sd[j + 1] - 1.0, vl, vh);
+                half_partials<0, HC>(tl, vl, vh, redA);
+            }
+        }
+        if (aj && warp >= HC && warp < 2 * HC) half_reduce<T>(redB, warp - HC, lane, sden[j], bcB);
+        PDAS_TRACE(3)
+        tl.sync();
+        PDAS_TRACE(4)
+        if (trace && j >= 8 && j < 24) g_casc_trace[((tslot * 16 + (j - 8)) * 6) + 5] = clock64();
+    }
+#undef PDAS_TRACE
+    // P(cnt): axpy B(cnt-1)
+    if (act(cnt - 1)) half_axpy<FULL, HC, HC>(tl, bcB, sptr(cnt - 1));
+    tl.sync();
+    if (tl.t == 0) mbar_arrive_a(pp.empty_a + 8 * ((k0 + cnt - 1) % S));
+    pp.k = k0 + cnt;
+}
+
+template <bool TMA, int S, int T, int R, int C, bool GEN>
+__device__ __forceinline__ void apply_global(Tile<T, R, C, GEN>& tl, Pipe<S>& pp,
+                                             const double* __restrict__ cols,
+                                             const double* __restrict__ a, idx_t base, idx_t l0,
+                                             idx_t l1, bool producer) {
+    const int cnt = (int)(l1 - l0);
+    if (cnt <= 0) return;
+    const int m = tl.m;
+    if (TMA && producer) {
+        const int pre = cnt < S ? cnt : S;
+        for (int i = 0; i < pre; ++i)
+            pipe_issue(pp, pp.k + i, cols + (l0 + i) * m, a + (l0 + i) * m, m);
+    }
+    // warp-uniform choice of the select-free path (every row of every lane exists)
+    if (!GEN && __all_sync(0xffffffffu, tl.full()))
+        apply_impl<TMA, true>(tl, pp, cols, a, base, l0, cnt, producer);
+    else
+        apply_impl<TMA, false>(tl, pp, cols, a, base, l0, cnt, producer);
+}
+
+// ------------------------------------------------------------ warp-specialized update
+// CTA = 2 compute warpgroups (256 threads: the register tile, T = 256) + 1
+// reducer warpgroup (128 threads: cross-thread reductions, divisions, TMA
+// producer, stage bookkeeping).  The tile's C columns are two halves A/B
+// skewed by half a pivot, so the compute warps always have fp64 work while
+// the reducer finishes the other half's serial chain:
+//   compute C1(j): axpy B(j-1), partials B(j)        -> arrive PB
+//   compute C2(j): axpy A(j),   partials A(j+1)      -> arrive PA
+//   reducer R1(j): reduce A(j) -> gA, stage j+1 ready -> arrive GA
+//   reducer R2(j): reduce B(j) -> gB                 -> arrive GB
+// v_j and P_j are carried in registers between the two uses; stage j is
+// recycled by the producer once PA(j+1) shows its last reader finished.
+// Named barriers (384 threads): 1 = PA, 2 = PB, 3 = GA, 4 = GB.
+constexpr int kWsT = 256;       // compute threads
+constexpr int kWsThreads = 384; // + reducer warpgroup
+constexpr int kWsRegsCompute = 232, kWsRegsReducer = 40;
+
+template <int S, int R, int C, bool FULL>
+__device__ __forceinline__ void ws_compute(Tile<kWsT, R, C, false>& tl, const double* buf, int mp,
+                                           const double* sd, int cnt, double* redA, double* redB,
+                                           const double* bcA, const double* bcB) {
+    constexpr int HC = C / 2, NT = kWsThreads;
+    const int stage = 2 * mp;
+    double vl[R], vh[R], pl[R], ph[R];
+    auto sptr = [&](int j) -> const double* { return buf + (j % S) * stage; };
+    auto act = [&](int j) { return sd[j] != 1.0; };
+    auto partials = [&](int h0, double* red) {
+#pragma unroll
+        for (int c = 0; c < HC; ++c) {
+            double s[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                double lo = vl[r] * tl.xl[r][h0 + c];
+                double hi = vh[r] * tl.xh[r][h0 + c];
+                s[r] = lo + hi;
+            }
+            red[c * kWsT + tl.t] = lane_tree<R>(s);
+        }
+    };
+    auto axpy = [&](int h0, const double* bc) {
+        double g[HC];
+#pragma unroll
+        for (int c = 0; c < HC; ++c) g[c] = bc[c];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const bool hi = FULL || tl.vhi(r);
+#pragma unroll
+            for (int c = 0; c < HC; ++c) {
+                double q0 = g[c] * pl[r];
+                tl.xl[r][h0 + c] = tl.xl[r][h0 + c] - q0;
+            }
+            if (hi) {
+#pragma unroll
+                for (int c = 0; c < HC; ++c) {
+                    double q1 = g[c] * ph[r];
+                    tl.xh[r][h0 + c] = tl.xh[r][h0 + c] - q1;
+                }
+            }
+        }
+    };
+    // GA(-1): stage 0 is ready
+    named_bar(3, NT);
+    if (act(0)) {
+        tl.template make_v<false, FULL>(sptr(0) + mp, sd[0] - 1.0, vl, vh);
+        partials(0, redA);
+    }
+    named_arrive(1, NT);
+    for (int j = 0; j < cnt; ++j) {
+        // ---- C1(j)
+        if (j > 0) {
+            named_bar(4, NT);
+            if (act(j - 1)) axpy(HC, bcB);
+        }
+        if (act(j)) partials(HC, redB);
+        named_arrive(2, NT);
+        // ---- C2(j)
+        named_bar(3, NT);  // gA(j) ready, stage j+1 ready
+        if (act(j)) {
+            tl.template load_p<false, FULL>(sptr(j), pl, ph);
+            axpy(0, bcA);
+        }
+        if (j + 1 < cnt && act(j + 1)) {
+            tl.template make_v<false, FULL>(sptr(j + 1) + mp, sd[j + 1] - 1.0, vl, vh);
+            partials(0, redA);
+        }
+        named_arrive(1, NT);
+    }
+    named_bar(4, NT);
+    if (act(cnt - 1)) axpy(HC, bcB);
+}
+
+template <int S, int R, int C>
+__device__ __forceinline__ void ws_reducer(Pipe<S>& pp, const double* __restrict__ cols,
+                                           const double* __restrict__ a, idx_t p0, int cnt, int m,
+                                           const double* redA, const double* redB, double* bcA,
+                                           double* bcB) {
+    constexpr int HC = C / 2, NT = kWsThreads, NW = kWsT / 32;
+    const int rt = threadIdx.x - kWsT;  // 0..127
+    const int w = rt >> 5, lane = rt & 31;
+    const bool producer = rt == 0;
+    const double* sd = pp.sd;
+    const double* sden = pp.sden;
+    auto wait_stage = [&](int j) {
+        if (producer) mbar_wait_a(pp.full_a + 8 * (j % S), (j / S) & 1u);
+    };
+    auto reduce = [&](const double* red, double* bc, double denom) {
+        for (int c = w; c < HC; c += 4) {
+            double q[NW];
+#pragma unroll
+            for (int k = 0; k < NW; ++k) q[k] = red[c * kWsT + lane + 32 * k];
+            const double v = warp_butterfly32(lane_tree<NW>(q));
+            const double g = v / denom;
+            if (lane == 0) bc[c] = g;
+        }
+    };
+    // prologue: stages 0 .. S-1 in flight; release the compute warps once
+    // stage 0 has landed (GA(-1))
+    if (producer)
+        for (int i = 0; i < (cnt < S ? cnt : S); ++i)
+            pipe_issue(pp, i, cols + (p0 + i) * m, a + (p0 + i) * m, m, false);
+    wait_stage(0);
+    named_arrive(3, NT);
+    for (int j = 0; j < cnt; ++j) {
+        // ---- R1(j)
+        named_bar(1, NT);  // partials A(j) published (C2(j-1) done: stage j-1 free)
+        if (j >= 1 && producer && j - 1 + S < cnt)
+            pipe_issue(pp, j - 1 + S, cols + (p0 + j - 1 + S) * m, a + (p0 + j - 1 + S) * m, m,
+                       false);
+        if (sd[j] != 1.0) reduce(redA, bcA, sden[j]);
+        if (j + 1 < cnt) wait_stage(j + 1);
+        named_arrive(3, NT);
+        // ---- R2(j)
+        named_bar(2, NT);  // partials B(j) published
+        if (sd[j] != 1.0) reduce(redB, bcB, sden[j]);
+        named_arrive(4, NT);
+    }
+    named_bar(1, NT);  // the compute warps' final PA arrival
+}
+
+// pipe_issue without the empty-barrier protocol (single producer that knows
+// from the named barriers when a stage is free): plain full-barrier refill.
+template <int S, int R, int C>
+__global__ void __launch_bounds__(kWsThreads, 1)
+    k_casc_update_ws(double* __restrict__ cols, const double* __restrict__ a,
+                     const double* __restrict__ d, const double* __restrict__ denoms, int m,
+                     idx_t n, idx_t p0, idx_t p1, idx_t tile0, const int32_t* __restrict__ fail) {
+    if (*(volatile const int32_t*)fail) return;
+    double *red, *bc;
+    Pipe<S> pp;
+    carve<kWsT, C, 1, S>(red, bc, pp, false, m);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(pp.full + s, 1);
+        mbar_fence_init();
+    }
+    stage_scalars(pp, d, denoms, p0, p0, p1, true);
+    __syncthreads();
+    const int cnt = (int)(p1 - p0);
+    constexpr int HC = C / 2;
+    double* redA = red;
+    double* redB = red + HC * kWsT;
+    double* bcA = bc;
+    double* bcB = bc + HC;
+    if (threadIdx.x >= kWsT) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kWsRegsReducer));
+        ws_reducer<S, R, C>(pp, cols, a, p0, cnt, m, redA, redB, bcA, bcB);
+        return;
+    }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kWsRegsCompute));
+    Tile<kWsT, R, C, false> tl;
+    tl.init(threadIdx.x, m, 0, red, bc);
+    const idx_t col0 = (tile0 + blockIdx.x) * C;
+    tl.load(cols, col0, n + 1);
+    if (__all_sync(0xffffffffu, tl.full()))
+        ws_compute<S, R, C, true>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
+    else
+        ws_compute<S, R, C, false>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
+    tl.store(cols, col0, n + 1);
 }
 
 // ------------------------------------------------------------ update kernel
 // Tile (tile0 + blockIdx.x) of CT = G*C columns receives pivots [p0, p1);
 // group g (T threads) owns columns [tile*CT + g*C, +C).
-template <bool TMA, int T, int R, int C, int G, bool GEN>
+template <bool TMA, int S, int T, int R, int C, int G, bool GEN>
 __global__ void __launch_bounds__(T* G, 1)
     k_casc_update(double* __restrict__ cols, const double* __restrict__ a,
                   const double* __restrict__ d, const double* __restrict__ denoms, int m, idx_t n,
-                  idx_t p0, idx_t p1, idx_t tile0, int S, const int32_t* __restrict__ fail) {
+                  idx_t p0, idx_t p1, idx_t tile0, const int32_t* __restrict__ fail) {
     if (*(volatile const int32_t*)fail) return;
     double *red, *bc;
-    Pipe pp;
-    carve<T, C, G>(red, bc, pp, TMA ? S : 0, m);
+    Pipe<S> pp;
+    carve<T, C, G, S>(red, bc, pp, TMA, m);
+    stage_scalars(pp, d, denoms, p0, p0, p1, true);
+    __syncthreads();
     const int grp = threadIdx.x / T;
     Tile<T, R, C, GEN> tl;
     tl.init(threadIdx.x % T, m, 1 + grp, red + grp * C * T, bc + grp * C);
     const idx_t col0 = (tile0 + blockIdx.x) * (C * G) + grp * C;
     tl.load(cols, col0, n + 1);
-    apply_global<TMA>(tl, pp, cols, a, d, denoms, p0, p1, threadIdx.x == 0);
+    if constexpr (TMA && G == 2 && !GEN && S >= 4) {
+        const int cnt = (int)(p1 - p0);
+        if (threadIdx.x == 0)
+            for (int i = 0; i < (cnt < S ? cnt : S); ++i)
+                pipe_issue(pp, pp.k + i, cols + (p0 + i) * m, a + (p0 + i) * m, m);
+        if (__all_sync(0xffffffffu, tl.full()))
+            apply_pingpong<S, true>(tl, pp, grp, cols, a, p0, cnt, threadIdx.x == 0);
+        else
+            apply_pingpong<S, false>(tl, pp, grp, cols, a, p0, cnt, threadIdx.x == 0);
+    } else if constexpr (TMA && G == 1 && !GEN && C % 2 == 0 && C / 2 <= T / 32 && S >= 3) {
+        const int cnt = (int)(p1 - p0);
+        if (g_casc_mode == 4) {
+            apply_global<TMA>(tl, pp, cols, a, p0, p0, p1, threadIdx.x == 0);
+        } else {
+            if (threadIdx.x == 0)
+                for (int i = 0; i < (cnt < S ? cnt : S); ++i)
+                    pipe_issue(pp, pp.k + i, cols + (p0 + i) * m, a + (p0 + i) * m, m);
+            if (__all_sync(0xffffffffu, tl.full()))
+                apply_split<S, true>(tl, pp, cols, a, p0, cnt, threadIdx.x == 0);
+            else
+                apply_split<S, false>(tl, pp, cols, a, p0, cnt, threadIdx.x == 0);
+        }
+    } else {
+        apply_global<TMA>(tl, pp, cols, a, p0, p0, p1, threadIdx.x == 0);
+    }
     tl.store(cols, col0, n + 1);
 }
 
 // ------------------------------------------------------------ panel kernel
-// One CTA per tile of block [p0, p1): apply the previous block [q0, q1),
+// One CTA per tile of block [p0, p1): apply the previous block [q0, p0),
 // then the pivots of this block's earlier tiles as their CTAs publish them
 // (flags[tile] == epoch), then the in-register triangle; publish.  Breakdown
 // is detected here, in step order, and reported as the 1-based step.
-template <bool TMA, int T, int R, int C, bool GEN>
+template <bool TMA, int S, int T, int R, int C, bool GEN>
 __global__ void __launch_bounds__(T, 1)
     k_casc_panel(double* __restrict__ cols, const double* __restrict__ a,
                  const double* __restrict__ d, double* __restrict__ denoms, int m, idx_t n,
-                 idx_t q0, idx_t q1, idx_t p0, idx_t p1, int S, int32_t* __restrict__ fail,
-                 int* __restrict__ flags, int epoch) {
+                 idx_t q0, idx_t p0, idx_t p1, int32_t* __restrict__ fail, int* __restrict__ flags,
+                 int epoch) {
     if (*(volatile int32_t*)fail) return;
     double *red, *bc;
-    Pipe pp;
-    carve<T, C, 1>(red, bc, pp, TMA ? S : 0, m);
+    Pipe<S> pp;
+    carve<T, C, 1, S>(red, bc, pp, TMA, m);
+    // d for [q0, p1) and the previous block's denominators, window base q0
+    stage_scalars(pp, d, denoms, q0, q0, p0, true);
+    for (idx_t l = p0 + threadIdx.x; l < p1; l += blockDim.x) pp.sd[l - q0] = __ldg(d + l);
+    __syncthreads();
     Tile<T, R, C, GEN> tl;
     tl.init(threadIdx.x, m, 1, red, bc);
     const bool producer = threadIdx.x == 0;
     const idx_t tile = p0 / C + blockIdx.x;
     const idx_t col0 = tile * C;
     tl.load(cols, col0, n + 1);
-    apply_global<TMA>(tl, pp, cols, a, d, denoms, q0, q1, producer);
+    apply_global<TMA>(tl, pp, cols, a, q0, q0, p0, producer);
     bool dead = false;
     for (idx_t tp = p0 / C; tp < tile; ++tp) {
         if (producer)
-            while (ld_acquire(flags + tp) != epoch) __nanosleep(64);
+            while (ld_acquire(flags + tp) != epoch) __nanosleep(32);
         __syncthreads();
         if (*(volatile int32_t*)fail) {
             dead = true;
             break;
         }
-        fence_proxy_async_global();  // peer CTA's generic stores -> our TMA reads
         const idx_t e = tp * C + C < p1 ? tp * C + C : p1;
-        apply_global<TMA>(tl, pp, cols, a, d, denoms, tp * C, e, producer);
+        if (threadIdx.x < C && tp * C + threadIdx.x < e)
+            pp.sden[tp * C + threadIdx.x - q0] = __ldcg(denoms + tp * C + threadIdx.x);
+        fence_proxy_async_global();  // peer CTA's generic stores -> our TMA reads
+        __syncthreads();
+        apply_global<TMA>(tl, pp, cols, a, q0, tp * C, e, producer);
     }
     if (!dead) {
         // triangle over this tile's own pivot columns, A columns via the pipe
         const int cnt = (int)((col0 + C < p1 ? col0 + C : p1) - col0);
         const unsigned k0 = pp.k;
         if (TMA && producer) {
-            const int pre = cnt < pp.S ? cnt : pp.S;
+            const int pre = cnt < S ? cnt : S;
             for (int i = 0; i < pre; ++i) pipe_issue(pp, k0 + i, nullptr, a + (col0 + i) * m, m);
         }
         bool broken = false;
@@ -436,26 +974,26 @@ __global__ void __launch_bounds__(T, 1)
             if (cl < cnt) {
                 const idx_t l = col0 + cl;
                 const unsigned use = k0 + cl;
-                const int s = (int)(use % pp.S);
                 const double* ac = a + l * m;
                 if (TMA) {
-                    mbar_wait(pp.full + s, (use / pp.S) & 1u);
+                    const int s = (int)(use % S);
+                    mbar_wait(pp.full + s, (use / S) & 1u);
                     ac = pp.buf + (size_t)s * 2 * pp.mp + pp.mp;
                 }
-                const double dl = __ldg(d + l);
+                const double dl = pp.sd[l - q0];
                 const bool active = dl != 1.0 && !broken;
                 double part[C];
                 if (active) {
                     double vl[R], vh[R];
-                    tl.template make_v<!TMA>(ac, dl - 1.0, vl, vh);
+                    tl.template make_v<!TMA, false>(ac, dl - 1.0, vl, vh);
                     tl.partials(vl, vh, part);
                     tl.publish(part);
                 }
                 tl.sync();
                 if (TMA && cl > 0) {
-                    if (producer) mbar_arrive(pp.empty + (int)((use - 1) % pp.S));
-                    if (producer && cl - 1 + pp.S < cnt)
-                        pipe_issue(pp, use - 1 + pp.S, nullptr, a + (l - 1 + pp.S) * m, m);
+                    if (producer) mbar_arrive(pp.empty + (int)((use - 1) % S));
+                    if (producer && cl - 1 + S < cnt)
+                        pipe_issue(pp, use - 1 + S, nullptr, a + (l - 1 + S) * m, m);
                 }
                 if (active) {
                     double inner[C];
@@ -493,7 +1031,7 @@ __global__ void __launch_bounds__(T, 1)
         }
         if (TMA) {
             tl.sync();
-            if (producer) mbar_arrive(pp.empty + (int)((k0 + cnt - 1) % pp.S));
+            if (producer) mbar_arrive(pp.empty + (int)((k0 + cnt - 1) % S));
             pp.k = k0 + cnt;
         }
         if (!broken) tl.store(cols, col0, n + 1);
@@ -508,23 +1046,33 @@ struct CascCfg {
     int T, R, Cu, G, CT;
 };
 
+static int env_int(const char* name, int dflt) {
+    const char* s = getenv(name);
+    return s && *s ? atoi(s) : dflt;
+}
+
 static CascCfg cascade_cfg(idx_t m) {
     const idx_t H = m > 1 ? pow2_ceil(m) >> 1 : 0;
+    const int variant = env_int("PDAS_CASCADE_VARIANT", 0);
     if (H <= 32) return {32, 1, 8, 1, 8};
     if (H == 64) return {64, 1, 8, 1, 8};
     if (H == 128) return {128, 1, 8, 1, 8};
     if (H == 256) return {256, 1, 8, 2, 16};
     if (H == 512) return {256, 2, 8, 2, 16};
-    if (H == 1024) return {256, 4, 4, 2, 8};
-    if (H == 2048) return {256, 8, 2, 2, 4};
-    if (H == 4096) return {256, 16, 1, 2, 2};
+    if (H == 1024) {
+        if (variant == 1) return {256, 4, 4, 2, 8};
+        if (variant == 2) return {256, 4, 8, 1, 8};
+        return {512, 2, 8, 1, 8};
+    }
+    if (H == 2048) return {256, 8, 4, 1, 4};
+    if (H == 4096) return {256, 16, 2, 1, 2};
     if (H == 8192) return {256, 32, 1, 1, 1};
     return {0, 0, 0, 0, 0};
 }
 
 idx_t cascade_supported_m() { return 16384; }
 
-// Side stream (high priority) + two events for the panel lookahead, per device.
+// Side stream (high priority) + events for the panel lookahead, per device.
 struct SideStream {
     cudaStream_t ps = nullptr;
     cudaEvent_t e0 = nullptr, eP = nullptr, eU = nullptr;
@@ -546,19 +1094,26 @@ static SideStream& side_stream() {
     return s;
 }
 
-template <bool TMA, int T, int R, int Cu, int G, int CT>
+template <bool TMA, int S, int T, int R, int Cu, int G, int CT>
 static int run_cascade_impl(double* cols, const double* a, const double* d, int m, idx_t n,
-                            double* denoms, int32_t* fail, int* flags, int epoch, int B, int S,
+                            double* denoms, int32_t* fail, int* flags, int epoch, int B,
                             cudaStream_t st) {
     constexpr bool GEN = (T == 32);
     static_assert(Cu * G == CT, "tile width");
-    B = (B + CT - 1) / CT * CT;
     const size_t smem_u = casc_smem_bytes<T, Cu, G>(TMA ? S : 0, m);
     const size_t smem_p = casc_smem_bytes<T, CT, 1>(TMA ? S : 0, m);
-    auto ku = k_casc_update<TMA, T, R, Cu, G, GEN>;
-    auto kp = k_casc_panel<TMA, T, R, CT, GEN>;
+    auto ku = k_casc_update<TMA, S, T, R, Cu, G, GEN>;
+    auto kp = k_casc_panel<TMA, S, T, R, CT, GEN>;
     cudaFuncSetAttribute(ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_u);
     cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
+    // warp-specialized update for the 256-thread single-group layouts
+    constexpr bool kUseWs = TMA && T == kWsT && G == 1 && CT % 2 == 0 && S >= 2;
+    constexpr int CW = kUseWs ? CT : 2;
+    auto kws = k_casc_update_ws<S, R, CW>;
+    const size_t smem_ws = casc_smem_bytes<kWsT, CW, 1>(S, m);
+    const bool use_ws = kUseWs && env_int("PDAS_CASCADE_WS", 1) != 0;
+    if (use_ws)
+        cudaFuncSetAttribute(kws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ws);
     const idx_t ntiles = (n + 1 + CT - 1) / CT;
     const idx_t nb = (n + B - 1) / B;
     auto blk_end = [&](idx_t b) { return (b + 1) * B < n ? (b + 1) * B : n; };
@@ -566,9 +1121,9 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
     SideStream& ss = side_stream();
     cudaEventRecord(ss.e0, st);
     cudaStreamWaitEvent(ss.ps, ss.e0, 0);
-    cudaEventRecord(ss.eU, st);  // "U_rest(-1)" = nothing beyond the start
-    kp<<<(unsigned)tiles_of(0), T, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, 0, 0, 0, blk_end(0),
-                                                    S, fail, flags, epoch);
+    cudaEventRecord(ss.eU, st);
+    kp<<<(unsigned)tiles_of(0), T, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, 0, 0, blk_end(0),
+                                                    fail, flags, epoch);
     cudaEventRecord(ss.eP, ss.ps);
     for (idx_t b = 0; b < nb; ++b) {
         cudaStreamWaitEvent(st, ss.eP, 0);  // panel(b): block b is final
@@ -576,16 +1131,20 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
             // panel(b+1) needs block b (stream order on ps) and U_rest(b-1)
             cudaStreamWaitEvent(ss.ps, ss.eU, 0);
             kp<<<(unsigned)tiles_of(b + 1), T, smem_p, ss.ps>>>(
-                cols, a, d, denoms, m, n, b * B, blk_end(b), (b + 1) * B, blk_end(b + 1), S, fail,
-                flags, epoch);
+                cols, a, d, denoms, m, n, b * B, (b + 1) * B, blk_end(b + 1), fail, flags, epoch);
             cudaEventRecord(ss.eP, ss.ps);
         }
         // U_rest(b): every tile beyond block b+1 (or beyond block b at the end)
         const idx_t last = b + 1 < nb ? blk_end(b + 1) : blk_end(b);
         const idx_t t0 = (last + CT - 1) / CT;
-        if (t0 < ntiles)
-            ku<<<(unsigned)(ntiles - t0), T * G, smem_u, st>>>(cols, a, d, denoms, m, n, b * B,
-                                                               blk_end(b), t0, S, fail);
+        if (t0 < ntiles) {
+            if (use_ws)
+                kws<<<(unsigned)(ntiles - t0), kWsThreads, smem_ws, st>>>(
+                    cols, a, d, denoms, m, n, b * B, blk_end(b), t0, fail);
+            else
+                ku<<<(unsigned)(ntiles - t0), T * G, smem_u, st>>>(cols, a, d, denoms, m, n, b * B,
+                                                                   blk_end(b), t0, fail);
+        }
         cudaEventRecord(ss.eU, st);
     }
     return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
@@ -595,22 +1154,28 @@ template <int T, int R, int Cu, int G, int CT>
 static int run_cascade(double* cols, const double* a, const double* d, int m, idx_t n,
                        double* denoms, int32_t* fail, int* flags, int epoch, int B,
                        cudaStream_t st) {
+    B = (B + CT - 1) / CT * CT;
+    if (B > kMaxBlock) B = kMaxBlock / CT * CT;
     const bool aligned = (m % 2 == 0) && (((uintptr_t)cols | (uintptr_t)a) % 16 == 0);
-    const size_t budget = 200 * 1024;
-    int S = 4;
-    while (S > 2 && casc_smem_bytes<T, CT, 1>(S, m) > budget) --S;
-    if (aligned && casc_smem_bytes<T, CT, 1>(S, m) <= budget &&
-        casc_smem_bytes<T, Cu, G>(S, m) <= budget)
-        return run_cascade_impl<true, T, R, Cu, G, CT>(cols, a, d, m, n, denoms, fail, flags,
-                                                       epoch, B, S, st);
-    return run_cascade_impl<false, T, R, Cu, G, CT>(cols, a, d, m, n, denoms, fail, flags, epoch,
-                                                    B, 1, st);
+    const size_t budget = 210 * 1024;
+    if (aligned && env_int("PDAS_CASCADE_STAGES", 5) >= 5 &&
+        casc_smem_bytes<T, CT, 1>(5, m) <= budget &&
+        casc_smem_bytes<T, Cu, G>(5, m) <= budget)
+        return run_cascade_impl<true, 5, T, R, Cu, G, CT>(cols, a, d, m, n, denoms, fail, flags,
+                                                          epoch, B, st);
+    if (aligned && casc_smem_bytes<T, CT, 1>(4, m) <= budget &&
+        casc_smem_bytes<T, Cu, G>(4, m) <= budget)
+        return run_cascade_impl<true, 4, T, R, Cu, G, CT>(cols, a, d, m, n, denoms, fail, flags,
+                                                          epoch, B, st);
+    if (aligned && casc_smem_bytes<T, CT, 1>(2, m) <= budget &&
+        casc_smem_bytes<T, Cu, G>(2, m) <= budget)
+        return run_cascade_impl<true, 2, T, R, Cu, G, CT>(cols, a, d, m, n, denoms, fail, flags,
+                                                          epoch, B, st);
+    return run_cascade_impl<false, 1, T, R, Cu, G, CT>(cols, a, d, m, n, denoms, fail, flags,
+                                                       epoch, B, st);
 }
 
-idx_t cascade_flags_count(idx_t m, idx_t n) {
-    CascCfg c = cascade_cfg(m);
-    return c.CT > 0 ? (n + 1 + c.CT - 1) / c.CT + 1 : 1;
-}
+idx_t cascade_flags_count(idx_t m, idx_t n) { return n + 2; }
 
 int launch_cascade(double* cols, const double* a, const double* d, idx_t m, idx_t n,
                    double* denoms, int32_t* fail_dev, int* flags, int epoch, int block_pivots,
@@ -619,7 +1184,16 @@ int launch_cascade(double* cols, const double* a, const double* d, idx_t m, idx_
     cudaMemsetAsync(fail_dev, 0, sizeof(int32_t), st);
     if (n == 0) return PDAS_OK;
     const CascCfg cfg = cascade_cfg(m);
-    const int B = block_pivots > 0 ? block_pivots : 64;
+    const int B = block_pivots > 0 ? block_pivots : env_int("PDAS_CASCADE_BLOCK", 64);
+    {
+        static int mode_set = -1;
+        const int mode = env_int("PDAS_CASCADE_MODE", 0);
+        if (mode != mode_set) {
+            cudaMemcpyToSymbolAsync(g_casc_mode, &mode, sizeof(int), 0, cudaMemcpyHostToDevice, st);
+            cudaStreamSynchronize(st);
+            mode_set = mode;
+        }
+    }
 #define PDAS_CASC(T_, R_, C_, G_, CT_)                                                       \
     if (cfg.T == T_ && cfg.R == R_ && cfg.Cu == C_ && cfg.G == G_)                           \
         return run_cascade<T_, R_, C_, G_, CT_>(cols, a, d, (int)m, n, denoms, fail_dev, flags, \
@@ -629,12 +1203,21 @@ int launch_cascade(double* cols, const double* a, const double* d, idx_t m, idx_
     PDAS_CASC(128, 1, 8, 1, 8)
     PDAS_CASC(256, 1, 8, 2, 16)
     PDAS_CASC(256, 2, 8, 2, 16)
+    PDAS_CASC(256, 4, 8, 1, 8)
     PDAS_CASC(256, 4, 4, 2, 8)
-    PDAS_CASC(256, 8, 2, 2, 4)
-    PDAS_CASC(256, 16, 1, 2, 2)
+    PDAS_CASC(512, 2, 8, 1, 8)
+    PDAS_CASC(256, 8, 4, 1, 4)
+    PDAS_CASC(256, 16, 2, 1, 2)
     PDAS_CASC(256, 32, 1, 1, 1)
 #undef PDAS_CASC
     return PDAS_ERR_UNSUPPORTED;
 }
 
 }  // namespace pdas
+
+// Debug only (not part of the ABI header): copy the clock64 trace out.
+extern "C" int pdas_debug_cascade_trace(long long* host_out, int count) {
+    if (count > 2 * 16 * 6) count = 2 * 16 * 6;
+    return cudaMemcpyFromSymbol(host_out, pdas::g_casc_trace, sizeof(long long) * count) ==
+                   cudaSuccess ? 0 : -2;
+}
