@@ -19,7 +19,6 @@ import json
 import os
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -41,6 +40,9 @@ def algorithmic(m, n):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
+    """One `nvidia-smi --query-gpu ... -lms 200` process for the whole timed
+    region (B200_PROFILING.md clocks line); parsed afterwards."""
+
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -48,30 +50,35 @@ class ClockSampler:
     def __init__(self, index=0):
         self.index = index
         self.rows = []
-        self._stop = threading.Event()
-        self._t = None
+        self.proc = None
+        self.path = os.path.join(REPO, "gpurun_out", f"clocks_{os.getpid()}.csv")
 
     def __enter__(self):
-        def run():
-            while not self._stop.is_set():
-                try:
-                    out = subprocess.run(
-                        ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                         "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                        timeout=5).stdout.strip()
-                    if out:
-                        self.rows.append([x.strip() for x in out.split(",")])
-                except Exception:
-                    pass
-                self._stop.wait(0.2)
-
-        self._t = threading.Thread(target=run, daemon=True)
-        self._t.start()
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.fh,
+                stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *exc):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+            for line in open(self.path):
+                parts = [x.strip() for x in line.strip().split(",")]
+                if len(parts) >= 8:
+                    self.rows.append(parts)
 
     def summary(self):
         if not self.rows:

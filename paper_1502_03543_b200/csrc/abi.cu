@@ -33,10 +33,28 @@ int check_cuda(int rc, const char* where) {
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Keep freed stream-ordered scratch in the device pool across synchronisations
+// (the default release threshold of 0 hands it back to the driver at every
+// sync, turning each per-call scratch allocation into a real allocation).
+void retain_pool() {
+    static thread_local int done[16] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    if (done[dev & 15]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    done[dev & 15] = 1;
+}
+
 template <class T>
 int scratch(T** p, size_t count, cudaStream_t st) {
     *p = nullptr;
     if (count == 0) return PDAS_OK;
+    retain_pool();
     if (cudaMallocAsync((void**)p, count * sizeof(T), st) != cudaSuccess) {
         cudaGetLastError();
         return set_err(PDAS_ERR_NOMEM, "cudaMallocAsync failed");

@@ -38,12 +38,6 @@
 
 namespace pdas {
 
-// Diagnostic ablation switch (PDAS_CASCADE_MODE): 0 = normal; 1 = skip the
-// cross-thread reduction; 2 = skip the per-thread partials.  Results are
-// wrong for modes != 0; used only by tools/cascade_time.py experiments.
-__device__ int g_casc_mode = 0;
-__device__ long long g_casc_trace[2 * 16 * 6];
-
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -393,16 +387,10 @@ __device__ __forceinline__ void apply_impl(Tile<T, R, C, GEN>& tl, Pipe<S>& pp,
     const double* ga = a + l0 * m;      // global A column of pivot l0 + j: ga + j*m
     const double* gc = cols + l0 * m;   // global P column
     const int stage = 2 * pp.mp;
-    const bool trace = g_casc_mode == 3 && blockIdx.x == 0 && l0 == 1280 &&
-                       (threadIdx.x == 0 || threadIdx.x == blockDim.x - 32);
-    const int tslot = threadIdx.x == 0 ? 0 : 1;
-#define PDAS_TRACE(pt)                                                              \
-    if (trace && j >= 8 && j < 24) g_casc_trace[((tslot * 16 + (j - 8)) * 6) + (pt)] = clock64();
     for (int j = 0; j < cnt; ++j) {
         const unsigned use = k0 + j;
         const double* pc;
         const double* ac;
-        PDAS_TRACE(0)
         if (TMA) {
             const uint32_t s = use % S;
             mbar_wait_a(pp.full_a + 8 * s, (use / S) & 1u);
@@ -412,7 +400,6 @@ __device__ __forceinline__ void apply_impl(Tile<T, R, C, GEN>& tl, Pipe<S>& pp,
             pc = gc + (size_t)j * m;
             ac = ga + (size_t)j * m;
         }
-        PDAS_TRACE(1)
         const double dl = sd[j];
         const bool active = dl != 1.0;
         double part[C];
@@ -422,7 +409,6 @@ __device__ __forceinline__ void apply_impl(Tile<T, R, C, GEN>& tl, Pipe<S>& pp,
             tl.partials(vl, vh, part);
             tl.publish(part);
         }
-        PDAS_TRACE(2)
         tl.sync();  // B1: partials published; stage of use-1 fully consumed
         if (TMA && j > 0) {
             if (tl.t == 0) mbar_arrive_a(pp.empty_a + 8 * ((use - 1) % S));
@@ -430,18 +416,14 @@ __device__ __forceinline__ void apply_impl(Tile<T, R, C, GEN>& tl, Pipe<S>& pp,
                 pipe_issue(pp, use - 1 + S, gc + (size_t)(j - 1 + S) * m,
                            ga + (size_t)(j - 1 + S) * m, m);
         }
-        PDAS_TRACE(3)
         if (active) {
             double g[C];
             tl.template finish<true>(part, sden[j], g);
-            PDAS_TRACE(4)
-            double pl[R], ph[R];
+                double pl[R], ph[R];
             tl.template load_p<!TMA, FULL>(pc, pl, ph);
             tl.template axpy<FULL>(g, pl, ph);
         }
-        PDAS_TRACE(5)
     }
-#undef PDAS_TRACE
     if (TMA) {
         tl.sync();
         if (tl.t == 0) mbar_arrive_a(pp.empty_a + 8 * ((k0 + cnt - 1) % S));
@@ -527,149 +509,6 @@ __device__ __forceinline__ void apply_pingpong(Tile<T, R, C, false>& tl, Pipe<S>
             mbar_arrive_a(pp.empty_a + 8 * ((pp.k + j) % S));
     }
     pp.k += cnt;
-}
-
-// ------------------------------------------------------------ split schedule
-// Half-tile skew (the update kernel's main path).  The tile's C columns are
-// two halves A = [0, C/2) and B = [C/2, C) processed half a pivot apart, so
-// each phase carries the fp64 work of one half while the reducer warps of the
-// other half run their serial chain (shared-memory hop, shuffles, division):
-//   P(j): axpy B(j-1), partials B(j), reduce A(j) [warps of half A] | barrier
-//   Q(j): axpy A(j),   partials A(j+1), reduce B(j) [warps of half B] | barrier
-// Every column still sees its pivots in ascending order with the reference
-// rounding sequence; only the interleaving of independent columns changes.
-template <int H0, int NH, int T, int R, int C>
-__device__ __forceinline__ void half_partials(const Tile<T, R, C, false>& tl, const double (&vl)[R],
-                                              const double (&vh)[R], double* red) {
-#pragma unroll
-    for (int c = 0; c < NH; ++c) {
-        double s[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            double lo = vl[r] * tl.xl[r][H0 + c];
-            double hi = vh[r] * tl.xh[r][H0 + c];
-            s[r] = lo + hi;
-        }
-        red[c * T + tl.t] = lane_tree<R>(s);
-    }
-}
-
-template <bool FULL, int H0, int NH, int T, int R, int C>
-__device__ __forceinline__ void half_axpy(Tile<T, R, C, false>& tl, const double* bc,
-                                          const double* pc) {
-    double g[NH];
-#pragma unroll
-    for (int c = 0; c < NH; ++c) g[c] = bc[c];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const bool hi = FULL || tl.vhi(r);
-        const double pl = pc[tl.row(r)];
-        const double ph = hi ? pc[tl.row(r) + tl.H] : 0.0;
-#pragma unroll
-        for (int c = 0; c < NH; ++c) {
-            double q0 = g[c] * pl;
-            tl.xl[r][H0 + c] = tl.xl[r][H0 + c] - q0;
-        }
-        if (hi) {
-#pragma unroll
-            for (int c = 0; c < NH; ++c) {
-                double q1 = g[c] * ph;
-                tl.xh[r][H0 + c] = tl.xh[r][H0 + c] - q1;
-            }
-        }
-    }
-}
-
-// Reducer warp for column c of a half: levels T/2 .. 1 then g = inner/denom.
-template <int T>
-__device__ __forceinline__ void half_reduce(const double* red, int c, int lane, double denom,
-                                            double* bc) {
-    constexpr int NW = T / 32;
-    double q[NW];
-#pragma unroll
-    for (int k = 0; k < NW; ++k) q[k] = red[c * T + lane + 32 * k];
-    const double v = warp_butterfly32(lane_tree<NW>(q));
-    if (lane == 0) bc[c] = v / denom;
-}
-
-template <int S, bool FULL, int T, int R, int C>
-__device__ __forceinline__ void apply_split(Tile<T, R, C, false>& tl, Pipe<S>& pp,
-                                            const double* __restrict__ cols,
-                                            const double* __restrict__ a, idx_t l0, int cnt,
-                                            bool producer) {
-    static_assert(C % 2 == 0 && C / 2 <= T / 32, "one reducer warp per half column");
-    constexpr int HC = C / 2;
-    const int m = tl.m;
-    const int warp = tl.t >> 5, lane = tl.t & 31;
-    double* redA = tl.red;
-    double* redB = tl.red + HC * T;
-    double* bcA = tl.bc;
-    double* bcB = tl.bc + HC;
-    const double* sd = pp.sd;  // window base == l0
-    const double* sden = pp.sden;
-    const double* ga = a + l0 * m;
-    const double* gc = cols + l0 * m;
-    const int stage = 2 * pp.mp;
-    const unsigned k0 = pp.k;
-    const bool trace = g_casc_mode == 3 && blockIdx.x == 0 && l0 == 1280 &&
-                       (threadIdx.x == 0 || threadIdx.x == blockDim.x - 32);
-    const int tslot = threadIdx.x == 0 ? 0 : 1;
-#define PDAS_TRACE(pt)                                                              \
-    if (trace && j >= 8 && j < 24) g_casc_trace[((tslot * 16 + (j - 8)) * 6) + (pt)] = clock64();
-    auto sptr = [&](int j) -> const double* { return pp.buf + ((k0 + j) % S) * stage; };
-    auto swait = [&](int j) { mbar_wait_a(pp.full_a + 8 * ((k0 + j) % S), ((k0 + j) / S) & 1u); };
-    auto act = [&](int j) { return sd[j] != 1.0; };
-    // Q(-1): partials A(0)
-    swait(0);
-    if (act(0)) {
-        double vl[R], vh[R];
-        tl.template make_v<false, FULL>(sptr(0) + pp.mp, sd[0] - 1.0, vl, vh);
-        half_partials<0, HC>(tl, vl, vh, redA);
-    }
-    tl.sync();
-    for (int j = 0; j < cnt; ++j) {
-        const bool aj = act(j);
-        PDAS_TRACE(0)
-        // ---- P(j)
-        if (j > 0 && act(j - 1)) half_axpy<FULL, HC, HC>(tl, bcB, sptr(j - 1));
-        if (aj) {
-            double vl[R], vh[R];
-            tl.template make_v<false, FULL>(sptr(j) + pp.mp, sd[j] - 1.0, vl, vh);
-            half_partials<HC, HC>(tl, vl, vh, redB);
-            if (warp < HC) half_reduce<T>(redA, warp, lane, sden[j], bcA);
-        }
-        PDAS_TRACE(1)
-        tl.sync();
-        PDAS_TRACE(2)
-        // stage j-1 had its last reader (axpy B) in P(j): recycle it
-        if (j > 0) {
-            if (tl.t == 0) mbar_arrive_a(pp.empty_a + 8 * ((k0 + j - 1) % S));
-            if (producer && j - 1 + S < cnt)
-                pipe_issue(pp, k0 + j - 1 + S, gc + (size_t)(j - 1 + S) * m,
-                           ga + (size_t)(j - 1 + S) * m, m);
-        }
-        // ---- Q(j)
-        if (aj) half_axpy<FULL, 0, HC>(tl, bcA, sptr(j));
-        if (j + 1 < cnt) {
-            swait(j + 1);
-            if (act(j + 1)) {
-                double vl[R], vh[R];
-                tl.template make_v<false, FULL>(sptr(j + 1) + pp.mp, sd[j + 1] - 1.0, vl, vh);
-                half_partials<0, HC>(tl, vl, vh, redA);
-            }
-        }
-        if (aj && warp >= HC && warp < 2 * HC) half_reduce<T>(redB, warp - HC, lane, sden[j], bcB);
-        PDAS_TRACE(3)
-        tl.sync();
-        PDAS_TRACE(4)
-        if (trace && j >= 8 && j < 24) g_casc_trace[((tslot * 16 + (j - 8)) * 6) + 5] = clock64();
-    }
-#undef PDAS_TRACE
-    // P(cnt): axpy B(cnt-1)
-    if (act(cnt - 1)) half_axpy<FULL, HC, HC>(tl, bcB, sptr(cnt - 1));
-    tl.sync();
-    if (tl.t == 0) mbar_arrive_a(pp.empty_a + 8 * ((k0 + cnt - 1) % S));
-    pp.k = k0 + cnt;
 }
 
 template <bool TMA, int S, int T, int R, int C, bool GEN>
@@ -899,19 +738,6 @@ __global__ void __launch_bounds__(T* G, 1)
             apply_pingpong<S, true>(tl, pp, grp, cols, a, p0, cnt, threadIdx.x == 0);
         else
             apply_pingpong<S, false>(tl, pp, grp, cols, a, p0, cnt, threadIdx.x == 0);
-    } else if constexpr (TMA && G == 1 && !GEN && C % 2 == 0 && C / 2 <= T / 32 && S >= 3) {
-        const int cnt = (int)(p1 - p0);
-        if (g_casc_mode == 4) {
-            apply_global<TMA>(tl, pp, cols, a, p0, p0, p1, threadIdx.x == 0);
-        } else {
-            if (threadIdx.x == 0)
-                for (int i = 0; i < (cnt < S ? cnt : S); ++i)
-                    pipe_issue(pp, pp.k + i, cols + (p0 + i) * m, a + (p0 + i) * m, m);
-            if (__all_sync(0xffffffffu, tl.full()))
-                apply_split<S, true>(tl, pp, cols, a, p0, cnt, threadIdx.x == 0);
-            else
-                apply_split<S, false>(tl, pp, cols, a, p0, cnt, threadIdx.x == 0);
-        }
     } else {
         apply_global<TMA>(tl, pp, cols, a, p0, p0, p1, threadIdx.x == 0);
     }
@@ -1058,12 +884,8 @@ static CascCfg cascade_cfg(idx_t m) {
     if (H == 64) return {64, 1, 8, 1, 8};
     if (H == 128) return {128, 1, 8, 1, 8};
     if (H == 256) return {256, 1, 8, 2, 16};
-    if (H == 512) return {256, 2, 8, 2, 16};
-    if (H == 1024) {
-        if (variant == 1) return {256, 4, 4, 2, 8};
-        if (variant == 2) return {256, 4, 8, 1, 8};
-        return {512, 2, 8, 1, 8};
-    }
+    if (H == 512) return variant == 1 ? CascCfg{256, 2, 8, 2, 16} : CascCfg{256, 2, 16, 1, 16};
+    if (H == 1024) return variant == 1 ? CascCfg{256, 4, 4, 2, 8} : CascCfg{256, 4, 8, 1, 8};
     if (H == 2048) return {256, 8, 4, 1, 4};
     if (H == 4096) return {256, 16, 2, 1, 2};
     if (H == 8192) return {256, 32, 1, 1, 1};
@@ -1184,16 +1006,7 @@ int launch_cascade(double* cols, const double* a, const double* d, idx_t m, idx_
     cudaMemsetAsync(fail_dev, 0, sizeof(int32_t), st);
     if (n == 0) return PDAS_OK;
     const CascCfg cfg = cascade_cfg(m);
-    const int B = block_pivots > 0 ? block_pivots : env_int("PDAS_CASCADE_BLOCK", 64);
-    {
-        static int mode_set = -1;
-        const int mode = env_int("PDAS_CASCADE_MODE", 0);
-        if (mode != mode_set) {
-            cudaMemcpyToSymbolAsync(g_casc_mode, &mode, sizeof(int), 0, cudaMemcpyHostToDevice, st);
-            cudaStreamSynchronize(st);
-            mode_set = mode;
-        }
-    }
+    const int B = block_pivots > 0 ? block_pivots : env_int("PDAS_CASCADE_BLOCK", 128);
 #define PDAS_CASC(T_, R_, C_, G_, CT_)                                                       \
     if (cfg.T == T_ && cfg.R == R_ && cfg.Cu == C_ && cfg.G == G_)                           \
         return run_cascade<T_, R_, C_, G_, CT_>(cols, a, d, (int)m, n, denoms, fail_dev, flags, \
@@ -1205,7 +1018,7 @@ int launch_cascade(double* cols, const double* a, const double* d, idx_t m, idx_
     PDAS_CASC(256, 2, 8, 2, 16)
     PDAS_CASC(256, 4, 8, 1, 8)
     PDAS_CASC(256, 4, 4, 2, 8)
-    PDAS_CASC(512, 2, 8, 1, 8)
+    PDAS_CASC(256, 2, 16, 1, 16)
     PDAS_CASC(256, 8, 4, 1, 4)
     PDAS_CASC(256, 16, 2, 1, 2)
     PDAS_CASC(256, 32, 1, 1, 1)
@@ -1215,9 +1028,3 @@ int launch_cascade(double* cols, const double* a, const double* d, idx_t m, idx_
 
 }  // namespace pdas
 
-// Debug only (not part of the ABI header): copy the clock64 trace out.
-extern "C" int pdas_debug_cascade_trace(long long* host_out, int count) {
-    if (count > 2 * 16 * 6) count = 2 * 16 * 6;
-    return cudaMemcpyFromSymbol(host_out, pdas::g_casc_trace, sizeof(long long) * count) ==
-                   cudaSuccess ? 0 : -2;
-}
