@@ -184,13 +184,19 @@ def run_ours(args):
     from paper_1502_03543_b200._lib import call
     from paper_1502_03543_b200.engine import DeviceProblem, DeviceSolver
 
+    shard = world > 1 and args.mode == "shard"
     # instance (identical bits to the reference generator) + one-time prepare
     lp, start = P.gen_random_feasible(M, N, SEED)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     prob = DeviceProblem.from_lp(lp)
     L0 = prob.validate()
-    eng = DeviceSolver(prob, "woodbury", 0.9, L0=L0)
+    if shard:
+        from paper_1502_03543_b200.dist import ShardedSolver
+
+        eng = ShardedSolver(prob, dist.group.WORLD, 0.9, L0=L0)
+    else:
+        eng = DeviceSolver(prob, "woodbury", 0.9, L0=L0)
     torch.cuda.synchronize()
     prepare_s = time.perf_counter() - t0
 
@@ -228,7 +234,9 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     ms_per_step = ms / args.steps
-    value = world * 1e3 / ms_per_step  # iterations/s summed over replicas
+    # shard: one LP over all ranks; replicas: iterations/s summed over ranks
+    jobs = 1 if shard else world
+    value = jobs * 1e3 / ms_per_step
 
     # ---- cascade alone (dominant kernels): CUDA events on its stream
     m, n = M, N
@@ -309,13 +317,15 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if shard else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": {"workload": f"c3 dense LP m={M} n={N} seed={SEED} (BASELINE configs[2]), "
                                "each step = PDAS iteration 1 from the generator's start",
                    "m": M, "n": N, "l2": "inputs larger than L2 ([Y|x] 320 MB + A + Y)",
-                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-                   "cascade_block_pivots": 64},
-        "e2e": {"value": world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                   "parallelism": (f"column-sharded cascade over {world} GPUs (dist.py)" if shard
+                                   else f"replicas x{world}" if world > 1 else "1 GPU"),
+                   "cascade_block_pivots": 128},
+        "e2e": {"value": jobs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "roofline": roofline,
@@ -349,6 +359,8 @@ def main():
     ap.add_argument("--cpu-sample-steps", type=int, default=200)
     ap.add_argument("--ref-sample-steps", type=int, default=200)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--mode", default="shard", choices=["shard", "replicas"],
+                    help="N>1: one LP column-sharded over the GPUs, or N independent LPs")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -118,6 +118,30 @@ int64_t pdas_cascade_ws_bytes(int64_t m, int64_t n);
 int pdas_solve_sweeps_ws(double* cols, const double* a, const double* d, int64_t m, int64_t n,
                          void* ws, int32_t epoch, int32_t* fail_dev, void* stream);
 
+/* Building blocks of the cascade for column-sharded (multi-GPU) execution,
+ * parallel.py:1-7 / the per-step column independence of _kernels.pyx:260-289.
+ * Pivots come in blocks of pdas_cascade_block_pivots(); columns in tiles of
+ * pdas_cascade_tile_width(m) (tile t = columns [t*w, t*w+w) of [Y|x]).
+ *
+ * panel: for block [p0, p1) whose tiles have had every pivot < q0 applied,
+ * apply the previous block [q0, p0) (denominators in ws), then run the
+ * block's own steps in order: after it, columns [p0, p1) are final, their
+ * denominators are in ws and a breakdown sets *fail_dev = l + 1.  The tiles
+ * touched are those covering [p0, p1) (including column n when it shares the
+ * last tile).  No-op when *fail_dev != 0 on entry.
+ *
+ * update: apply pivots [p0, p1) (final columns + denominators already in
+ * cols/ws) to the listed tiles (device int64 array, any order, each tile past
+ * p1).  No-op when *fail_dev != 0.  ws/epoch follow pdas_solve_sweeps_ws. */
+int pdas_cascade_tile_width(int64_t m);
+int pdas_cascade_block_pivots(void);
+int pdas_cascade_panel(double* cols, const double* a, const double* d, int64_t m, int64_t n,
+                       int64_t q0, int64_t p0, int64_t p1, void* ws, int32_t epoch,
+                       int32_t* fail_dev, void* stream);
+int pdas_cascade_update(double* cols, const double* a, const double* d, int64_t m, int64_t n,
+                        int64_t p0, int64_t p1, const int64_t* tiles_dev, int64_t ntiles,
+                        void* ws, int32_t* fail_dev, void* stream);
+
 /* cholesky_solve (linalg.py:126-132) for ONE right-hand side, in place on
  * x (m): the per-iteration x0 = L0^-T L0^-1 (A x) of init_workspace
  * (normal.py:123).  Same rounding sequence as cholesky_solve_many with k=1,

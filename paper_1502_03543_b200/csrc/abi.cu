@@ -194,6 +194,57 @@ int pdas_solve_sweeps_ws(double* cols, const double* a, const double* d, int64_t
         "solve_sweeps");
 }
 
+int pdas_cascade_tile_width(int64_t m) {
+    if (m < 1 || m > pdas::cascade_supported_m()) return 0;
+    return pdas::cascade_tile_width(m);
+}
+
+int pdas_cascade_block_pivots(void) { return pdas::kCascadeBlock; }
+
+static int split_ws(void* ws, int64_t n, double** denoms, int** flags) {
+    const int64_t nd = n > 0 ? n : 1;
+    *denoms = static_cast<double*>(ws);
+    *flags = reinterpret_cast<int*>(static_cast<unsigned char*>(ws) + ((nd * 8 + 255) / 256) * 256);
+    return 0;
+}
+
+int pdas_cascade_panel(double* cols, const double* a, const double* d, int64_t m, int64_t n,
+                       int64_t q0, int64_t p0, int64_t p1, void* ws, int32_t epoch,
+                       int32_t* fail_dev, void* stream) {
+    if (m < 1 || n < 1 || fail_dev == nullptr || ws == nullptr || epoch < 1)
+        return set_err(PDAS_ERR_ARG, "cascade_panel: bad args");
+    if (m > pdas::cascade_supported_m())
+        return set_err(PDAS_ERR_UNSUPPORTED, "cascade_panel: m above the compiled configurations");
+    const int ct = pdas::cascade_tile_width(m);
+    if (q0 < 0 || q0 > p0 || p0 >= p1 || p1 > n || p0 % ct != 0 || q0 % ct != 0 ||
+        p1 - p0 > pdas::kCascadeBlock || p0 - q0 > pdas::kCascadeBlock)
+        return set_err(PDAS_ERR_ARG, "cascade_panel: block bounds");
+    double* denoms;
+    int* flags;
+    split_ws(ws, n, &denoms, &flags);
+    return check_cuda(pdas::launch_cascade_panel(cols, a, d, m, n, q0, p0, p1, denoms, fail_dev,
+                                                 flags, epoch, S(stream)),
+                      "cascade_panel");
+}
+
+int pdas_cascade_update(double* cols, const double* a, const double* d, int64_t m, int64_t n,
+                        int64_t p0, int64_t p1, const int64_t* tiles_dev, int64_t ntiles,
+                        void* ws, int32_t* fail_dev, void* stream) {
+    if (m < 1 || n < 1 || fail_dev == nullptr || ws == nullptr || ntiles < 0 ||
+        (ntiles > 0 && tiles_dev == nullptr))
+        return set_err(PDAS_ERR_ARG, "cascade_update: bad args");
+    if (m > pdas::cascade_supported_m())
+        return set_err(PDAS_ERR_UNSUPPORTED, "cascade_update: m above the compiled configurations");
+    if (p0 < 0 || p0 >= p1 || p1 > n || p1 - p0 > pdas::kCascadeBlock)
+        return set_err(PDAS_ERR_ARG, "cascade_update: block bounds");
+    double* denoms;
+    int* flags;
+    split_ws(ws, n, &denoms, &flags);
+    return check_cuda(pdas::launch_cascade_update(cols, a, d, m, n, p0, p1, tiles_dev, ntiles,
+                                                  denoms, fail_dev, S(stream)),
+                      "cascade_update");
+}
+
 int pdas_cholesky_solve_one(const double* low, int64_t m, double* x, void* stream) {
     if (m < 1) return set_err(PDAS_ERR_ARG, "cholesky_solve_one: bad shape");
     double* work = nullptr;

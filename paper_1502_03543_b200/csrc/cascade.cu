@@ -676,7 +676,8 @@ template <int S, int R, int C>
 __global__ void __launch_bounds__(kWsThreads, 1)
     k_casc_update_ws(double* __restrict__ cols, const double* __restrict__ a,
                      const double* __restrict__ d, const double* __restrict__ denoms, int m,
-                     idx_t n, idx_t p0, idx_t p1, idx_t tile0, const int32_t* __restrict__ fail) {
+                     idx_t n, idx_t p0, idx_t p1, idx_t tile0, const int32_t* __restrict__ fail,
+                     const int64_t* __restrict__ tiles) {
     if (*(volatile const int32_t*)fail) return;
     double *red, *bc;
     Pipe<S> pp;
@@ -701,7 +702,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kWsRegsCompute));
     Tile<kWsT, R, C, false> tl;
     tl.init(threadIdx.x, m, 0, red, bc);
-    const idx_t col0 = (tile0 + blockIdx.x) * C;
+    const idx_t col0 = (tiles ? tiles[blockIdx.x] : tile0 + blockIdx.x) * C;
     tl.load(cols, col0, n + 1);
     if (__all_sync(0xffffffffu, tl.full()))
         ws_compute<S, R, C, true>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
@@ -717,7 +718,8 @@ template <bool TMA, int S, int T, int R, int C, int G, bool GEN>
 __global__ void __launch_bounds__(T* G, 1)
     k_casc_update(double* __restrict__ cols, const double* __restrict__ a,
                   const double* __restrict__ d, const double* __restrict__ denoms, int m, idx_t n,
-                  idx_t p0, idx_t p1, idx_t tile0, const int32_t* __restrict__ fail) {
+                  idx_t p0, idx_t p1, idx_t tile0, const int32_t* __restrict__ fail,
+                  const int64_t* __restrict__ tiles) {
     if (*(volatile const int32_t*)fail) return;
     double *red, *bc;
     Pipe<S> pp;
@@ -727,7 +729,7 @@ __global__ void __launch_bounds__(T* G, 1)
     const int grp = threadIdx.x / T;
     Tile<T, R, C, GEN> tl;
     tl.init(threadIdx.x % T, m, 1 + grp, red + grp * C * T, bc + grp * C);
-    const idx_t col0 = (tile0 + blockIdx.x) * (C * G) + grp * C;
+    const idx_t col0 = (tiles ? tiles[blockIdx.x] : tile0 + blockIdx.x) * (C * G) + grp * C;
     tl.load(cols, col0, n + 1);
     if constexpr (TMA && G == 2 && !GEN && S >= 4) {
         const int cnt = (int)(p1 - p0);
@@ -916,10 +918,20 @@ static SideStream& side_stream() {
     return s;
 }
 
+// What to launch: the full cascade, or one building block of the sharded
+// cascade (dist.py): a panel over block [p0,p1) after previous block [q0,p0),
+// or an update of a tile list with block [p0,p1).
+struct CascOp {
+    int kind = 0;  // 0 full, 1 panel, 2 update
+    idx_t q0 = 0, p0 = 0, p1 = 0;
+    const int64_t* tiles = nullptr;
+    idx_t ntiles = 0;
+};
+
 template <bool TMA, int S, int T, int R, int Cu, int G, int CT>
 static int run_cascade_impl(double* cols, const double* a, const double* d, int m, idx_t n,
                             double* denoms, int32_t* fail, int* flags, int epoch, int B,
-                            cudaStream_t st) {
+                            cudaStream_t st, const CascOp& op) {
     constexpr bool GEN = (T == 32);
     static_assert(Cu * G == CT, "tile width");
     const size_t smem_u = casc_smem_bytes<T, Cu, G>(TMA ? S : 0, m);
@@ -929,14 +941,34 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
     cudaFuncSetAttribute(ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_u);
     cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
     // warp-specialized update for the 256-thread single-group layouts
-    constexpr bool kUseWs = TMA && T == kWsT && G == 1 && CT % 2 == 0 && S >= 2;
+    // (R >= 16 spills the compute warpgroups' 232-register budget)
+    constexpr bool kUseWs = TMA && T == kWsT && G == 1 && CT % 2 == 0 && S >= 2 && R <= 8;
     constexpr int CW = kUseWs ? CT : 2;
-    auto kws = k_casc_update_ws<S, R, CW>;
+    constexpr int RW = kUseWs ? R : 1;
+    auto kws = k_casc_update_ws<S, RW, CW>;
     const size_t smem_ws = casc_smem_bytes<kWsT, CW, 1>(S, m);
     const bool use_ws = kUseWs && env_int("PDAS_CASCADE_WS", 1) != 0;
     if (use_ws)
         cudaFuncSetAttribute(kws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ws);
     const idx_t ntiles = (n + 1 + CT - 1) / CT;
+    if (op.kind == 1) {
+        if (op.p0 % CT || op.p1 <= op.p0 || op.p1 - op.q0 > 2 * kMaxBlock) return PDAS_ERR_ARG;
+        kp<<<(unsigned)((op.p1 - op.p0 + CT - 1) / CT), T, smem_p, st>>>(
+            cols, a, d, denoms, m, n, op.q0, op.p0, op.p1, fail, flags, epoch);
+        return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
+    }
+    if (op.kind == 2) {
+        if (op.p1 - op.p0 > kMaxBlock || op.p1 <= op.p0) return PDAS_ERR_ARG;
+        if (op.ntiles > 0) {
+            if (use_ws)
+                kws<<<(unsigned)op.ntiles, kWsThreads, smem_ws, st>>>(
+                    cols, a, d, denoms, m, n, op.p0, op.p1, 0, fail, op.tiles);
+            else
+                ku<<<(unsigned)op.ntiles, T * G, smem_u, st>>>(cols, a, d, denoms, m, n, op.p0,
+                                                               op.p1, 0, fail, op.tiles);
+        }
+        return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
+    }
     const idx_t nb = (n + B - 1) / B;
     auto blk_end = [&](idx_t b) { return (b + 1) * B < n ? (b + 1) * B : n; };
     auto tiles_of = [&](idx_t b) { return (blk_end(b) - b * B + CT - 1) / CT; };
@@ -962,10 +994,10 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         if (t0 < ntiles) {
             if (use_ws)
                 kws<<<(unsigned)(ntiles - t0), kWsThreads, smem_ws, st>>>(
-                    cols, a, d, denoms, m, n, b * B, blk_end(b), t0, fail);
+                    cols, a, d, denoms, m, n, b * B, blk_end(b), t0, fail, nullptr);
             else
                 ku<<<(unsigned)(ntiles - t0), T * G, smem_u, st>>>(cols, a, d, denoms, m, n, b * B,
-                                                                   blk_end(b), t0, fail);
+                                                                   blk_end(b), t0, fail, nullptr);
         }
         cudaEventRecord(ss.eU, st);
     }
@@ -975,7 +1007,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
 template <int T, int R, int Cu, int G, int CT>
 static int run_cascade(double* cols, const double* a, const double* d, int m, idx_t n,
                        double* denoms, int32_t* fail, int* flags, int epoch, int B,
-                       cudaStream_t st) {
+                       cudaStream_t st, const CascOp& op) {
     B = (B + CT - 1) / CT * CT;
     if (B > kMaxBlock) B = kMaxBlock / CT * CT;
     const bool aligned = (m % 2 == 0) && (((uintptr_t)cols | (uintptr_t)a) % 16 == 0);
@@ -984,33 +1016,31 @@ static int run_cascade(double* cols, const double* a, const double* d, int m, id
         casc_smem_bytes<T, CT, 1>(5, m) <= budget &&
         casc_smem_bytes<T, Cu, G>(5, m) <= budget)
         return run_cascade_impl<true, 5, T, R, Cu, G, CT>(cols, a, d, m, n, denoms, fail, flags,
-                                                          epoch, B, st);
+                                                          epoch, B, st, op);
     if (aligned && casc_smem_bytes<T, CT, 1>(4, m) <= budget &&
         casc_smem_bytes<T, Cu, G>(4, m) <= budget)
         return run_cascade_impl<true, 4, T, R, Cu, G, CT>(cols, a, d, m, n, denoms, fail, flags,
-                                                          epoch, B, st);
+                                                          epoch, B, st, op);
     if (aligned && casc_smem_bytes<T, CT, 1>(2, m) <= budget &&
         casc_smem_bytes<T, Cu, G>(2, m) <= budget)
         return run_cascade_impl<true, 2, T, R, Cu, G, CT>(cols, a, d, m, n, denoms, fail, flags,
-                                                          epoch, B, st);
+                                                          epoch, B, st, op);
     return run_cascade_impl<false, 1, T, R, Cu, G, CT>(cols, a, d, m, n, denoms, fail, flags,
-                                                       epoch, B, st);
+                                                       epoch, B, st, op);
 }
 
 idx_t cascade_flags_count(idx_t m, idx_t n) { return n + 2; }
 
-int launch_cascade(double* cols, const double* a, const double* d, idx_t m, idx_t n,
-                   double* denoms, int32_t* fail_dev, int* flags, int epoch, int block_pivots,
-                   cudaStream_t st) {
-    if (m < 1 || n < 0 || m > INT_MAX / 4) return PDAS_ERR_ARG;
-    cudaMemsetAsync(fail_dev, 0, sizeof(int32_t), st);
-    if (n == 0) return PDAS_OK;
+int cascade_tile_width(idx_t m) { return cascade_cfg(m).CT; }
+
+static int dispatch_cascade(double* cols, const double* a, const double* d, idx_t m, idx_t n,
+                            double* denoms, int32_t* fail_dev, int* flags, int epoch, int B,
+                            cudaStream_t st, const CascOp& op) {
     const CascCfg cfg = cascade_cfg(m);
-    const int B = block_pivots > 0 ? block_pivots : env_int("PDAS_CASCADE_BLOCK", 128);
 #define PDAS_CASC(T_, R_, C_, G_, CT_)                                                       \
     if (cfg.T == T_ && cfg.R == R_ && cfg.Cu == C_ && cfg.G == G_)                           \
         return run_cascade<T_, R_, C_, G_, CT_>(cols, a, d, (int)m, n, denoms, fail_dev, flags, \
-                                                epoch, B, st);
+                                                epoch, B, st, op);
     PDAS_CASC(32, 1, 8, 1, 8)
     PDAS_CASC(64, 1, 8, 1, 8)
     PDAS_CASC(128, 1, 8, 1, 8)
@@ -1024,6 +1054,41 @@ int launch_cascade(double* cols, const double* a, const double* d, idx_t m, idx_
     PDAS_CASC(256, 32, 1, 1, 1)
 #undef PDAS_CASC
     return PDAS_ERR_UNSUPPORTED;
+}
+
+int launch_cascade(double* cols, const double* a, const double* d, idx_t m, idx_t n,
+                   double* denoms, int32_t* fail_dev, int* flags, int epoch, int block_pivots,
+                   cudaStream_t st) {
+    if (m < 1 || n < 0 || m > INT_MAX / 4) return PDAS_ERR_ARG;
+    cudaMemsetAsync(fail_dev, 0, sizeof(int32_t), st);
+    if (n == 0) return PDAS_OK;
+    const int B = block_pivots > 0 ? block_pivots : env_int("PDAS_CASCADE_BLOCK", 128);
+    return dispatch_cascade(cols, a, d, m, n, denoms, fail_dev, flags, epoch, B, st, CascOp{});
+}
+
+int launch_cascade_panel(double* cols, const double* a, const double* d, idx_t m, idx_t n,
+                         idx_t q0, idx_t p0, idx_t p1, double* denoms, int32_t* fail_dev,
+                         int* flags, int epoch, cudaStream_t st) {
+    if (m < 1 || m > INT_MAX / 4 || q0 < 0 || q0 > p0 || p1 > n) return PDAS_ERR_ARG;
+    CascOp op;
+    op.kind = 1;
+    op.q0 = q0;
+    op.p0 = p0;
+    op.p1 = p1;
+    return dispatch_cascade(cols, a, d, m, n, denoms, fail_dev, flags, epoch, kMaxBlock, st, op);
+}
+
+int launch_cascade_update(double* cols, const double* a, const double* d, idx_t m, idx_t n,
+                          idx_t p0, idx_t p1, const int64_t* tiles, idx_t ntiles, double* denoms,
+                          int32_t* fail_dev, cudaStream_t st) {
+    if (m < 1 || m > INT_MAX / 4 || p0 < 0 || p1 > n || ntiles < 0) return PDAS_ERR_ARG;
+    CascOp op;
+    op.kind = 2;
+    op.p0 = p0;
+    op.p1 = p1;
+    op.tiles = tiles;
+    op.ntiles = ntiles;
+    return dispatch_cascade(cols, a, d, m, n, denoms, fail_dev, nullptr, 0, kMaxBlock, st, op);
 }
 
 }  // namespace pdas

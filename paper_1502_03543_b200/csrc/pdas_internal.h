@@ -69,8 +69,16 @@ int launch_sweep_phase2(double* cols, idx_t m, idx_t l0, const double* inner, do
 int launch_cascade(double* cols, const double* a, const double* d, idx_t m, idx_t n,
                    double* denoms, int32_t* fail_dev, int* flags, int epoch, int block_pivots,
                    cudaStream_t st);
+int launch_cascade_panel(double* cols, const double* a, const double* d, idx_t m, idx_t n,
+                         idx_t q0, idx_t p0, idx_t p1, double* denoms, int32_t* fail_dev,
+                         int* flags, int epoch, cudaStream_t st);
+int launch_cascade_update(double* cols, const double* a, const double* d, idx_t m, idx_t n,
+                          idx_t p0, idx_t p1, const int64_t* tiles, idx_t ntiles, double* denoms,
+                          int32_t* fail_dev, cudaStream_t st);
 idx_t cascade_supported_m();
 idx_t cascade_flags_count(idx_t m, idx_t n);
+int cascade_tile_width(idx_t m);
+constexpr int kCascadeBlock = 128;  // pivots per block (= kMaxBlock in cascade.cu)
 
 // solve_kernels.cu (single right-hand side, latency-optimised)
 int launch_solve_one(const double* low, idx_t m, double* x, double* work, cudaStream_t st);

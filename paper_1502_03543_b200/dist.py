@@ -1,0 +1,363 @@
+"""Column-sharded Egidi-Maponi cascade: one process per GPU.
+
+Why it shards (reference parallel.py:1-7, _kernels.pyx:260-289, SURVEY.md
+§8(e)): inside step l every column k > l of [Y | x] is updated independently;
+the only cross-column input is the pivot column l (final after step l-1) and
+its denominator.  So columns can live on different GPUs as long as each
+finished pivot column reaches every GPU before that GPU applies it.
+
+Ownership (block-cyclic, aligned with the kernels' tiles):
+  * pivot block b = pivots [bB, min(bB+B, n)), B = pdas_cascade_block_pivots()
+    (128), owned by rank b mod G;
+  * column tile t = columns [tw, tw+w) of [Y | x], w = pdas_cascade_tile_width(m),
+    owned by the owner of the block its first column falls in (B is a multiple
+    of w, so a block's tiles are exactly its columns; the x column n belongs to
+    block n div B).
+Every rank holds the whole [Y | x] buffer -- Y and x0 are computed redundantly
+(deterministic, no exchange) -- but advances only the tiles it owns.
+
+Schedule of one cascade on every rank (`cascade_schedule`):
+    panel(0) on owner(0); broadcast block 0
+    for b = 0 .. nb-1:
+        main stream waits for block b
+        side stream: panel(b+1) on owner(b+1) (after its own update(b-1));
+                     broadcast block b+1                       (lookahead)
+        main stream: update(b) = block b applied to this rank's tiles past
+                     block b+1 (past block b at the end)
+    broadcast the x column from its owner (unless the last panel covered it)
+A block broadcast carries the block's final columns, its denominators and the
+fail word, so a breakdown found by the owner of its block stops every rank and
+all ranks return the same 1-based step.
+
+Parity: each column receives the pivots in ascending order with the same
+per-column arithmetic (tree dot, IEEE divide, unfused multiply-subtract), so
+the sharded result is bitwise the 1-GPU cascade (and the reference's) for any
+G, B and w (tests/test_dist.py on CPU with gloo, tests/test_gpu_dist.py with
+the CUDA blocks).
+
+The schedule is a generator that yields at every collective; the driver
+performs it.  `run_collective` does it with torch.distributed (NCCL on GPUs,
+gloo in the CPU tests); `run_lockstep` drives G in-process virtual ranks in
+lock-step (the broadcast becomes a copy), which is how one GPU checks the
+sharded path without running ranks that wait on each other.
+"""
+
+from __future__ import annotations
+
+import bisect
+import contextlib
+from typing import Iterator, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from .engine import DeviceSolver
+
+Op = Tuple  # ("block", b, src, c0, c1, p0, p1) | ("x", src)
+
+
+class ShardPlan:
+    """Block-cyclic ownership of pivots and column tiles for one rank."""
+
+    def __init__(self, m: int, n: int, world: int, rank: int, block: int, tile: int):
+        if world < 1 or not 0 <= rank < world:
+            raise ValueError("bad world/rank")
+        if tile < 1 or block < tile or block % tile:
+            raise ValueError("block must be a positive multiple of the tile width")
+        if n < 1:
+            raise ValueError("n must be >= 1")
+        self.m, self.n, self.world, self.rank = int(m), int(n), int(world), int(rank)
+        self.B, self.w = int(block), int(tile)
+        self.nb = (self.n + self.B - 1) // self.B
+        self.ntiles = (self.n + 1 + self.w - 1) // self.w
+        self.tiles = np.array([t for t in range(self.ntiles) if self.tile_owner(t) == rank],
+                              dtype=np.int64)
+        self._tl = self.tiles.tolist()
+        # the last panel's tiles cover column n unless n falls on a tile edge
+        self.x_in_last_panel = self.n % self.w != 0
+        self.x_owner = self.tile_owner(self.n // self.w)
+
+    def block_owner(self, b: int) -> int:
+        return b % self.world
+
+    def tile_owner(self, t: int) -> int:
+        return ((t * self.w) // self.B) % self.world
+
+    def owns_block(self, b: int) -> bool:
+        return self.block_owner(b) == self.rank
+
+    def block(self, b: int) -> Tuple[int, int]:
+        p0 = b * self.B
+        return p0, min(p0 + self.B, self.n)
+
+    def panel_bounds(self, b: int) -> Tuple[int, int, int]:
+        """(q0, p0, p1): block b after the previous block [q0, p0)."""
+        p0, p1 = self.block(b)
+        return (p0 - self.B if b > 0 else 0), p0, p1
+
+    def block_columns(self, b: int) -> Tuple[int, int]:
+        """Columns a panel over block b finalises (its tiles, clipped at n+1)."""
+        p0, p1 = self.block(b)
+        return p0, min((p1 + self.w - 1) // self.w * self.w, self.n + 1)
+
+    def update_start(self, b: int) -> int:
+        """Index into `tiles` of the first tile update(b) touches."""
+        last = self.block(b + 1)[1] if b + 1 < self.nb else self.block(b)[1]
+        t0 = (last + self.w - 1) // self.w
+        return bisect.bisect_left(self._tl, t0)
+
+    def block_op(self, b: int) -> Op:
+        c0, c1 = self.block_columns(b)
+        p0, p1 = self.block(b)
+        return ("block", b, self.block_owner(b), c0, c1, p0, p1)
+
+
+class _NullBackend:
+    """Stream hooks are no-ops unless a backend overrides them."""
+
+    def begin(self) -> None:
+        pass
+
+    def side(self):
+        return contextlib.nullcontext()
+
+    def main_wait_side(self) -> None:
+        pass
+
+    def side_wait_update(self) -> None:
+        pass
+
+    def mark_update(self) -> None:
+        pass
+
+
+def cascade_schedule(plan: ShardPlan, be) -> Iterator[Op]:
+    """One sharded cascade on this rank; yields each collective (see module doc).
+
+    `be` provides panel(q0, p0, p1), update(p0, p1, i0) (tiles plan.tiles[i0:])
+    and the stream hooks of _NullBackend."""
+    be.begin()
+    with be.side():
+        if plan.owns_block(0):
+            be.panel(*plan.panel_bounds(0))
+        yield plan.block_op(0)
+    for b in range(plan.nb):
+        be.main_wait_side()  # block b is final here
+        if b + 1 < plan.nb:
+            with be.side():
+                if plan.owns_block(b + 1):
+                    be.side_wait_update()  # this rank's update(b-1) reached block b+1
+                    be.panel(*plan.panel_bounds(b + 1))
+                yield plan.block_op(b + 1)
+        i0 = plan.update_start(b)
+        if i0 < len(plan.tiles):
+            be.update(*plan.block(b), i0)
+        be.mark_update()
+    be.main_wait_side()
+    if not plan.x_in_last_panel:
+        yield ("x", plan.x_owner)
+
+
+# ------------------------------------------------------------------ drivers
+def run_collective(plan: ShardPlan, be, group=None) -> None:
+    """Drive the schedule with torch.distributed broadcasts over `group`.
+
+    `be.block_views(c0, c1, p0, p1)` returns the tensors a block broadcast
+    carries (columns, denominators, fail word); `be.x_view()` the x column.
+    Each broadcast is issued under the stream the schedule is on."""
+    import torch.distributed as dist
+
+    ranks = None if group is None else dist.get_process_group_ranks(group)
+
+    def g(src):
+        return src if ranks is None else ranks[src]
+
+    for op in cascade_schedule(plan, be):
+        if op[0] == "block":
+            _, b, src, c0, c1, p0, p1 = op
+            for t in be.block_views(c0, c1, p0, p1):
+                dist.broadcast(t, g(src), group=group)
+        else:
+            dist.broadcast(be.x_view(), g(op[1]), group=group)
+
+
+def run_lockstep(plans: Sequence[ShardPlan], bes: Sequence) -> None:
+    """Drive G virtual ranks in one process: every rank advances to its next
+    collective, then the owner's views are copied into the others'."""
+    gens = [cascade_schedule(p, be) for p, be in zip(plans, bes)]
+    while True:
+        ops = [next(gn, None) for gn in gens]
+        if all(o is None for o in ops):
+            return
+        if any(o != ops[0] for o in ops):
+            raise RuntimeError(f"virtual ranks diverged: {ops}")
+        op = ops[0]
+        if op[0] == "block":
+            _, b, src, c0, c1, p0, p1 = op
+            srcv = bes[src].block_views(c0, c1, p0, p1)
+            for r, be in enumerate(bes):
+                if r != src:
+                    for dst, s in zip(be.block_views(c0, c1, p0, p1), srcv):
+                        dst.copy_(s)
+        else:
+            src = op[1]
+            for r, be in enumerate(bes):
+                if r != src:
+                    be.x_view().copy_(bes[src].x_view())
+
+
+# ------------------------------------------------------------------ CUDA backend
+class CudaShard(_NullBackend):
+    """The CUDA building blocks (pdas_cascade_panel / pdas_cascade_update) on
+    one rank's buffers.  cols: flat m*(n+1) fp64; a: flat m*n; d: n; ws: the
+    pdas_cascade_ws_bytes workspace (zeroed once); fail: 4-byte device view.
+
+    streams=True: panels + block broadcasts on a high-priority side stream,
+    updates on the caller's stream (the lookahead of the 1-GPU cascade)."""
+
+    def __init__(self, plan: ShardPlan, cols, a, d, ws, fail, streams: bool = True):
+        from . import _device as dv
+        from ._lib import call
+
+        t = dv.require_gpu()
+        self.t, self.dv, self.call = t, dv, call
+        self.plan = plan
+        self.cols, self.a, self.d, self.ws, self.fail = cols, a, d, ws, fail
+        nd = max(plan.n, 1)
+        self.denoms = ws[: nd * 8].view(t.float64)
+        self.tiles = t.from_numpy(plan.tiles.copy()).to(dv.device())
+        self.epoch = 0
+        self.streams = streams
+        if streams:
+            lo, hi = t.cuda.Stream.priority_range()
+            self.side_stream = t.cuda.Stream(priority=hi)
+            self.ev_update = t.cuda.Event()
+        self.main = None
+
+    def reset(self, cols, d):
+        self.cols, self.d = cols, d
+
+    # -- stream hooks
+    def begin(self) -> None:
+        self.epoch += 1
+        self.fail.zero_()
+        if self.streams:
+            self.main = self.t.cuda.current_stream()
+            self.side_stream.wait_stream(self.main)
+            self.ev_update.record(self.main)
+
+    def side(self):
+        return self.t.cuda.stream(self.side_stream) if self.streams else contextlib.nullcontext()
+
+    def main_wait_side(self) -> None:
+        if self.streams:
+            self.main.wait_stream(self.side_stream)
+
+    def side_wait_update(self) -> None:
+        if self.streams:
+            self.side_stream.wait_event(self.ev_update)
+
+    def mark_update(self) -> None:
+        if self.streams:
+            self.ev_update.record(self.main)
+
+    # -- compute
+    def panel(self, q0: int, p0: int, p1: int) -> None:
+        p, dv = self.plan, self.dv
+        self.call("pdas_cascade_panel", dv.ptr(self.cols), dv.ptr(self.a), dv.ptr(self.d), p.m,
+                  p.n, q0, p0, p1, dv.ptr(self.ws), self.epoch, dv.ptr(self.fail), dv.stream())
+
+    def update(self, p0: int, p1: int, i0: int) -> None:
+        p, dv = self.plan, self.dv
+        self.call("pdas_cascade_update", dv.ptr(self.cols), dv.ptr(self.a), dv.ptr(self.d), p.m,
+                  p.n, p0, p1, dv.ptr(self.tiles) + 8 * i0, len(p.tiles) - i0, dv.ptr(self.ws),
+                  dv.ptr(self.fail), dv.stream())
+
+    # -- collective payloads
+    def block_views(self, c0, c1, p0, p1):
+        m = self.plan.m
+        return [self.cols[c0 * m:c1 * m], self.denoms[p0:p1], self.fail]
+
+    def x_view(self):
+        m, n = self.plan.m, self.plan.n
+        return self.cols[n * m:(n + 1) * m]
+
+
+def cascade_tile_width(m: int) -> int:
+    from ._lib import load
+
+    w = int(load().pdas_cascade_tile_width(m))
+    if w < 1:
+        raise ValueError(f"no cascade configuration for m={m}")
+    return w
+
+
+def cascade_block_pivots() -> int:
+    from ._lib import load
+
+    return int(load().pdas_cascade_block_pivots())
+
+
+def make_plan(m: int, n: int, world: int, rank: int, block: Optional[int] = None) -> ShardPlan:
+    w = cascade_tile_width(m)
+    B = block or cascade_block_pivots()
+    return ShardPlan(m, n, world, rank, B, w)
+
+
+class ShardedSolver(DeviceSolver):
+    """DeviceSolver whose cascade runs column-sharded over a process group
+    (one process per GPU, NCCL).  Everything else of the iteration -- scaling,
+    A x, x0, A^T dy, ratio test, update -- is replicated on every rank (same
+    kernels, same bits), so the only traffic is the cascade's block
+    broadcasts plus one x-column broadcast per iteration."""
+
+    def __init__(self, prob, group=None, rho: float = 0.9, basis=None, L0=None,
+                 block: Optional[int] = None):
+        import torch.distributed as dist
+
+        from ._lib import OFF_CASCADE_FAIL
+
+        super().__init__(prob, "woodbury", rho, basis=basis, L0=L0)
+        self.group = group
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        self.plan = make_plan(self.m, self.n, world, rank, block)
+        fail = self.state[OFF_CASCADE_FAIL:OFF_CASCADE_FAIL + 4]
+        self.shard = CudaShard(self.plan, self.cols, prob.A, self.d, self.casc_ws, fail)
+        p = self.plan
+        self._casc_launches = sum(1 for b in range(p.nb) if p.owns_block(b)) + sum(
+            1 for b in range(p.nb) if p.update_start(b) < len(p.tiles))
+
+    def _cascade(self) -> None:
+        run_collective(self.plan, self.shard, self.group)
+        self.launches += self._casc_launches
+
+
+def solve_sweeps_virtual(cols: np.ndarray, a: np.ndarray, d: np.ndarray, world: int,
+                         block: Optional[int] = None) -> Tuple[int, List[np.ndarray]]:
+    """The sharded cascade over `world` virtual ranks on the current GPU, in
+    lock-step (no rank waits on another inside a kernel).  Returns the common
+    fail code and every rank's final [Y | x] (host copies, column-major).
+    Verification entry point for the multi-GPU schedule."""
+    from . import _device as dv
+    from ._lib import load
+
+    t = dv.require_gpu()
+    m, n = a.shape
+    A = dv.upload(np.asfortranarray(a))
+    dd = dv.upload(np.ascontiguousarray(d, dtype=np.float64))
+    wsb = int(load().pdas_cascade_ws_bytes(m, n))
+    plans, bes = [], []
+    for r in range(world):
+        plan = make_plan(m, n, world, r, block)
+        c = dv.upload(np.asfortranarray(cols))
+        ws = t.zeros(wsb, dtype=t.uint8, device=dv.device())
+        fail = t.zeros(1, dtype=t.int32, device=dv.device())
+        plans.append(plan)
+        bes.append(CudaShard(plan, c, A, dd, ws, fail, streams=False))
+    run_lockstep(plans, bes)
+    dv.synchronize()
+    fails = [int(be.fail.item()) for be in bes]
+    if len(set(fails)) != 1:
+        raise RuntimeError(f"ranks disagree on the breakdown step: {fails}")
+    outs = [dv.download(be.cols).reshape((m, n + 1), order="F") for be in bes]
+    return fails[0], outs

@@ -236,6 +236,14 @@ class DeviceSolver:
              dv.ptr(self.y), n, m, self._sptr(), st)
         self.launches += 7
 
+    def _cascade(self) -> None:
+        """solve_sweeps on [Y | x] (normal.py:124), fail word into the state."""
+        m, n = self.m, self.n
+        self.epoch += 1
+        call("pdas_solve_sweeps_ws", dv.ptr(self.cols), dv.ptr(self.prob.A), dv.ptr(self.d), m,
+             n, dv.ptr(self.casc_ws), self.epoch, self._sptr(OFF_CASCADE_FAIL), dv.stream())
+        self.launches += 2 * ((n + 127) // 128)
+
     def enqueue_solve(self) -> None:
         """Scaling, rhs and the normal-equations solve (cascade or direct)."""
         st = dv.stream()
@@ -249,12 +257,10 @@ class DeviceSolver:
             B = self.basis
             self.cols[:m * n].copy_(B.Y, non_blocking=True)  # init_workspace (normal.py:121-123)
             self.xcol.copy_(self.rhs, non_blocking=True)
-            d_solve_many(B.L0, m, self.xcol, 1)
-            self.epoch += 1
-            call("pdas_solve_sweeps_ws", dv.ptr(self.cols), dv.ptr(P.A), dv.ptr(self.d), m, n,
-                 dv.ptr(self.casc_ws), self.epoch, self._sptr(OFF_CASCADE_FAIL), st)
+            d_solve_many(B.L0, m, self.xcol, 1)  # k_fwd_one + k_bwd_one
+            self.launches += 2
+            self._cascade()
             self.dy = self.xcol
-            self.launches += 2 + 2 * ((n + 63) // 64)
         else:
             self._solve_direct_into(self.dy_direct, self._sptr(OFF_CHOL_FAIL))
             self.dy = self.dy_direct

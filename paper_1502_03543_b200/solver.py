@@ -260,12 +260,19 @@ def solve_lp(
     lp: StandardFormLP,
     start: InteriorPoint,
     opts: Optional[SolveOptions] = None,
+    *,
+    group=None,
 ) -> Tuple[InteriorPoint, Status, List[TraceRecord]]:
     """Run the affine-scaling iteration from a strictly feasible start.
 
     Returns the final iterate, a termination status and one trace record per
     completed iteration (solver.py:197-279).  Backend failures that survive
     the direct fallback surface as NUMERICAL_BREAKDOWN with the partial trace.
+
+    group: a torch.distributed process group (one process per GPU, every rank
+    calling with the same problem): the Woodbury cascade then runs
+    column-sharded over the group (dist.py); results are bitwise the 1-GPU
+    ones on every rank.
     """
     opts = opts or SolveOptions()
     prob = DeviceProblem.from_lp(lp)
@@ -274,7 +281,13 @@ def solve_lp(
     check_interior(p)
     _check_feasible_device(lp, prob, p)
     resolve_workers(opts.workers)
-    eng = DeviceSolver(prob, opts.backend, opts.rho, L0=L0 if opts.backend == "woodbury" else None)
+    if group is not None and opts.backend == "woodbury":
+        from .dist import ShardedSolver
+
+        eng = ShardedSolver(prob, group, opts.rho, L0=L0)
+    else:
+        eng = DeviceSolver(prob, opts.backend, opts.rho,
+                           L0=L0 if opts.backend == "woodbury" else None)
     eng.load_iterate(p.x, p.y, p.s)
     st0 = eng.objectives()
     gap = st0.gap
