@@ -183,6 +183,13 @@ int pdas_iter_objectives(const double* x, const double* s, const double* c, cons
  * Time it with events on `stream` to get the roofline denominator. */
 int pdas_probe_fp64(double* sink, int64_t iters, int64_t* ops, void* stream);
 
+/* The cascade divides every column's inner product by the step denominator
+ * with the reciprocal refinement hoisted per pivot (common.cuh div_by); this
+ * writes that result and the plain IEEE a/b side by side for n operand pairs
+ * so tests can check they are the same bits. */
+int pdas_selftest_div(const double* a, const double* b, int64_t n, double* out_fast,
+                      double* out_ref, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

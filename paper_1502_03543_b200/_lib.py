@@ -85,6 +85,7 @@ SIGNATURES = {
     "pdas_iter_update": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _VP, _VP]),
     "pdas_iter_objectives": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _I64, _I64, _VP, _VP]),
     "pdas_probe_fp64": (ctypes.c_int, [_VP, _I64, _VP, _VP]),
+    "pdas_selftest_div": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
 }
 
 _LIB = None

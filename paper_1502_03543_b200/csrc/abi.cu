@@ -321,4 +321,12 @@ int pdas_probe_fp64(double* sink, int64_t iters, int64_t* ops, void* stream) {
     return check_cuda(rc, "probe_fp64");
 }
 
+int pdas_selftest_div(const double* a, const double* b, int64_t n, double* out_fast,
+                      double* out_ref, void* stream) {
+    if (n < 0 || (n > 0 && (!a || !b || !out_fast || !out_ref)))
+        return set_err(PDAS_ERR_ARG, "selftest_div: bad args");
+    return check_cuda(pdas::launch_div_selftest(a, b, n, out_fast, out_ref, S(stream)),
+                      "selftest_div");
+}
+
 }  // extern "C"

@@ -36,6 +36,16 @@
 #include "pdas_internal.h"
 #include "tma.cuh"
 
+#ifndef PDAS_HOIST_WS
+#define PDAS_HOIST_WS 0
+#endif
+#ifndef PDAS_HOIST_TRI
+#define PDAS_HOIST_TRI 0
+#endif
+#ifndef PDAS_HOIST_FIN
+#define PDAS_HOIST_FIN 1
+#endif
+
 namespace pdas {
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
@@ -211,7 +221,7 @@ struct Tile {
     // divides), else out[c] = inner[c].  Ends with the group barrier when
     // T > 32; every thread returns all C values.
     template <bool DIV>
-    __device__ __forceinline__ void finish(const double (&part)[C], double denom,
+    __device__ __forceinline__ void finish(const double (&part)[C], double denom, double y,
                                            double (&out)[C]) const {
         const int lane = t & 31;
         if (T == 32) {
@@ -220,7 +230,7 @@ struct Tile {
             for (int c = 0; c < C; ++c) {
                 double v = warp_butterfly(part[c], w);
                 if (GEN && H < 32) v = __shfl_sync(0xffffffffu, v, 0);
-                out[c] = DIV ? v / denom : v;
+                out[c] = DIV ? (PDAS_HOIST_FIN ? div_by(v, denom, y) : v / denom) : v;
             }
         } else {
             constexpr int NW = T / 32;
@@ -230,7 +240,7 @@ struct Tile {
 #pragma unroll
                 for (int k = 0; k < NW; ++k) q[k] = red[c * T + lane + 32 * k];
                 double v = warp_butterfly32(lane_tree<NW>(q));
-                if (lane == 0) bc[c] = DIV ? v / denom : v;
+                if (lane == 0) bc[c] = DIV ? (PDAS_HOIST_FIN ? div_by(v, denom, y) : v / denom) : v;
             }
             sync();
 #pragma unroll
@@ -281,6 +291,7 @@ struct Pipe {
     unsigned k;
     double* sd;    // d[l - base] for the kernel's pivot window (shared memory)
     double* sden;  // denom[l - base]
+    double* sy;    // div_recip(denom[l - base]) (common.cuh)
 };
 
 __device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
@@ -324,10 +335,10 @@ __device__ __forceinline__ void pipe_issue(Pipe<S>& p, unsigned use, const doubl
 }
 
 // dynamic smem: red[G][C*T] | bc[G][C] | sd[2*kMaxBlock] | sden[2*kMaxBlock]
-//               | full[S] | empty[S] | stages
+//               | sy[2*kMaxBlock] | full[S] | empty[S] | stages
 template <int T, int C, int G>
 __host__ __device__ constexpr size_t casc_head_bytes(int S) {
-    return (((size_t)G * C * T + (size_t)G * C + 4 * kMaxBlock + 2 * (size_t)S) * sizeof(double) +
+    return (((size_t)G * C * T + (size_t)G * C + 6 * kMaxBlock + 2 * (size_t)S) * sizeof(double) +
             127) & ~(size_t)127;
 }
 
@@ -344,7 +355,8 @@ __device__ __forceinline__ void carve(double*& red, double*& bc, Pipe<S>& pp, bo
     bc = red + G * C * T;
     pp.sd = bc + G * C;
     pp.sden = pp.sd + 2 * kMaxBlock;
-    pp.full = reinterpret_cast<uint64_t*>(pp.sden + 2 * kMaxBlock);
+    pp.sy = pp.sden + 2 * kMaxBlock;
+    pp.full = reinterpret_cast<uint64_t*>(pp.sy + 2 * kMaxBlock);
     pp.empty = pp.full + S;
     pp.buf = reinterpret_cast<double*>(smem_raw + casc_head_bytes<T, C, G>(S));
     pp.full_a = smem_addr(pp.full);
@@ -368,7 +380,9 @@ __device__ __forceinline__ void stage_scalars(Pipe<S>& pp, const double* __restr
                                               idx_t lo, idx_t hi, bool with_d) {
     for (idx_t l = lo + threadIdx.x; l < hi; l += blockDim.x) {
         if (with_d) pp.sd[l - base] = __ldg(d + l);
-        pp.sden[l - base] = __ldcg(denoms + l);
+        const double den = __ldcg(denoms + l);
+        pp.sden[l - base] = den;
+        pp.sy[l - base] = div_recip(den);
     }
 }
 
@@ -384,6 +398,7 @@ __device__ __forceinline__ void apply_impl(Tile<T, R, C, GEN>& tl, Pipe<S>& pp,
     const unsigned k0 = pp.k;
     const double* sd = pp.sd + (l0 - base);
     const double* sden = pp.sden + (l0 - base);
+    const double* sy = pp.sy + (l0 - base);
     const double* ga = a + l0 * m;      // global A column of pivot l0 + j: ga + j*m
     const double* gc = cols + l0 * m;   // global P column
     const int stage = 2 * pp.mp;
@@ -418,8 +433,8 @@ __device__ __forceinline__ void apply_impl(Tile<T, R, C, GEN>& tl, Pipe<S>& pp,
         }
         if (active) {
             double g[C];
-            tl.template finish<true>(part, sden[j], g);
-                double pl[R], ph[R];
+            tl.template finish<true>(part, sden[j], sy[j], g);
+            double pl[R], ph[R];
             tl.template load_p<!TMA, FULL>(pc, pl, ph);
             tl.template axpy<FULL>(g, pl, ph);
         }
@@ -497,7 +512,7 @@ __device__ __forceinline__ void apply_pingpong(Tile<T, R, C, false>& tl, Pipe<S>
         if (producer && j >= 3 && j - 3 + S < cnt)
             pipe_issue(pp, pp.k + j - 3 + S, gc + (size_t)(j - 3 + S) * m,
                        ga + (size_t)(j - 3 + S) * m, m);
-        if (active) tl.template finish<true>(part, sden[j], g);
+        if (active) tl.template finish<true>(part, sden[j], pp.sy[j], g);
         prev_active = active;
         prev_pc = pc;
     }
@@ -544,9 +559,38 @@ __device__ __forceinline__ void apply_global(Tile<T, R, C, GEN>& tl, Pipe<S>& pp
 // v_j and P_j are carried in registers between the two uses; stage j is
 // recycled by the producer once PA(j+1) shows its last reader finished.
 // Named barriers (384 threads): 1 = PA, 2 = PB, 3 = GA, 4 = GB.
+#ifndef PDAS_ISSUE_LATE
+#define PDAS_ISSUE_LATE 1
+#endif
+#ifndef PDAS_PREFETCH_ACT
+#define PDAS_PREFETCH_ACT 1
+#endif
+#ifndef PDAS_WS_EARLY
+#define PDAS_WS_EARLY 0
+#endif
 constexpr int kWsT = 256;       // compute threads
 constexpr int kWsThreads = 384; // + reducer warpgroup
 constexpr int kWsRegsCompute = 232, kWsRegsReducer = 40;
+
+// Diagnostic build only (make variant VDEFS=-DPDAS_WS_TRACE=1): clock64 marks
+// of compute thread 0 / reducer thread 0 of one CTA per pivot, read back with
+// pdas_debug_ws_trace (tools/ws_trace.py).
+#ifndef PDAS_WS_TRACE
+#define PDAS_WS_TRACE 0
+#endif
+#if PDAS_WS_TRACE
+__device__ long long g_ws_trace[2][kMaxBlock][6];
+#define WS_MARK(who, j, k)                                                                   \
+    do {                                                                                     \
+        if (gridDim.x >= 300 && blockIdx.x == 150 && (threadIdx.x == 0 || threadIdx.x == kWsT) && \
+            (j) < kMaxBlock)                                                                 \
+            g_ws_trace[who][j][k] = clock64();                                               \
+    } while (0)
+#else
+#define WS_MARK(who, j, k) \
+    do {                   \
+    } while (0)
+#endif
 
 template <int S, int R, int C, bool FULL>
 __device__ __forceinline__ void ws_compute(Tile<kWsT, R, C, false>& tl, const double* buf, int mp,
@@ -593,33 +637,210 @@ __device__ __forceinline__ void ws_compute(Tile<kWsT, R, C, false>& tl, const do
     };
     // GA(-1): stage 0 is ready
     named_bar(3, NT);
-    if (act(0)) {
+    bool a_prev = false, a_cur = act(0);
+    if (a_cur) {
         tl.template make_v<false, FULL>(sptr(0) + mp, sd[0] - 1.0, vl, vh);
         partials(0, redA);
     }
     named_arrive(1, NT);
     for (int j = 0; j < cnt; ++j) {
+#if PDAS_PREFETCH_ACT
+        // d of pivot j+1, read before the barriers it would otherwise follow
+        const double dn = sd[j + 1 < cnt ? j + 1 : j];
+        const bool a_next = j + 1 < cnt && dn != 1.0;
+#endif
         // ---- C1(j)
+        WS_MARK(0, j, 0);
         if (j > 0) {
             named_bar(4, NT);
-            if (act(j - 1)) axpy(HC, bcB);
+            WS_MARK(0, j, 1);
+            if (a_prev) axpy(HC, bcB);
         }
-        if (act(j)) partials(HC, redB);
+        if (a_cur) partials(HC, redB);
         named_arrive(2, NT);
+        WS_MARK(0, j, 2);
         // ---- C2(j)
         named_bar(3, NT);  // gA(j) ready, stage j+1 ready
-        if (act(j)) {
+        WS_MARK(0, j, 3);
+#if !PDAS_PREFETCH_ACT
+        const double dn = sd[j + 1 < cnt ? j + 1 : j];
+        const bool a_next = j + 1 < cnt && dn != 1.0;
+#endif
+        if (a_cur) {
             tl.template load_p<false, FULL>(sptr(j), pl, ph);
             axpy(0, bcA);
         }
-        if (j + 1 < cnt && act(j + 1)) {
-            tl.template make_v<false, FULL>(sptr(j + 1) + mp, sd[j + 1] - 1.0, vl, vh);
+        if (a_next) {
+            tl.template make_v<false, FULL>(sptr(j + 1) + mp, dn - 1.0, vl, vh);
             partials(0, redA);
         }
         named_arrive(1, NT);
+        WS_MARK(0, j, 4);
+        a_prev = a_cur;
+        a_cur = a_next;
     }
     named_bar(4, NT);
-    if (act(cnt - 1)) axpy(HC, bcB);
+    if (a_prev) axpy(HC, bcB);
+}
+
+// Same schedule with the stage reads hoisted one phase earlier: right after
+// GB(j-1), C1(j) issues the shared-memory loads of P_j and A_{j+1} into
+// registers, so C2(j) starts on arithmetic (the reducer makes stage j+1
+// ready before GB(j-1) instead of before GA(j)).
+template <int S, int R, int C, bool FULL>
+__device__ __forceinline__ void ws_compute_early(Tile<kWsT, R, C, false>& tl, const double* buf,
+                                                 int mp, const double* sd, int cnt, double* redA,
+                                                 double* redB, const double* bcA,
+                                                 const double* bcB) {
+    constexpr int HC = C / 2, NT = kWsThreads;
+    const int stage = 2 * mp;
+    double vl[R], vh[R], pl[R], ph[R];
+    double nl[R], nh[R], al[R], ah[R];  // P_j and raw A_{j+1}, loaded ahead
+    auto sptr = [&](int j) -> const double* { return buf + (j % S) * stage; };
+    auto partials = [&](int h0, double* red) {
+#pragma unroll
+        for (int c = 0; c < HC; ++c) {
+            double s[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                double lo = vl[r] * tl.xl[r][h0 + c];
+                double hi = vh[r] * tl.xh[r][h0 + c];
+                s[r] = lo + hi;
+            }
+            red[c * kWsT + tl.t] = lane_tree<R>(s);
+        }
+    };
+    auto axpy = [&](int h0, const double* bc) {
+        double g[HC];
+#pragma unroll
+        for (int c = 0; c < HC; ++c) g[c] = bc[c];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const bool hi = FULL || tl.vhi(r);
+#pragma unroll
+            for (int c = 0; c < HC; ++c) {
+                double q0 = g[c] * pl[r];
+                tl.xl[r][h0 + c] = tl.xl[r][h0 + c] - q0;
+            }
+            if (hi) {
+#pragma unroll
+                for (int c = 0; c < HC; ++c) {
+                    double q1 = g[c] * ph[r];
+                    tl.xh[r][h0 + c] = tl.xh[r][h0 + c] - q1;
+                }
+            }
+        }
+    };
+    // GA(-1): stages 0 and 1 are ready
+    named_bar(3, NT);
+    bool a_prev = false, a_cur = sd[0] != 1.0;
+    if (a_cur) {
+        tl.template make_v<false, FULL>(sptr(0) + mp, sd[0] - 1.0, vl, vh);
+        partials(0, redA);
+    }
+    named_arrive(1, NT);
+    for (int j = 0; j < cnt; ++j) {
+        const double dn = sd[j + 1 < cnt ? j + 1 : j];
+        const bool a_next = j + 1 < cnt && dn != 1.0;
+        // ---- C1(j)
+        WS_MARK(0, j, 0);
+        if (j > 0) named_bar(4, NT);  // gB(j-1) ready, stages j and j+1 ready
+        WS_MARK(0, j, 1);
+        if (a_cur) tl.template load_p<false, FULL>(sptr(j), nl, nh);
+        if (a_next) tl.template load_p<false, FULL>(sptr(j + 1) + mp, al, ah);
+        if (j > 0 && a_prev) axpy(HC, bcB);
+        if (a_cur) partials(HC, redB);
+        named_arrive(2, NT);
+        WS_MARK(0, j, 2);
+        // ---- C2(j)
+        named_bar(3, NT);  // gA(j) ready
+        WS_MARK(0, j, 3);
+        if (a_cur) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                pl[r] = nl[r];
+                ph[r] = nh[r];
+            }
+            axpy(0, bcA);
+        }
+        if (a_next) {
+            const double f = dn - 1.0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                vl[r] = al[r] * f;
+                vh[r] = (FULL || tl.vhi(r)) ? ah[r] * f : 0.0;
+            }
+            partials(0, redA);
+        }
+        named_arrive(1, NT);
+        WS_MARK(0, j, 4);
+        a_prev = a_cur;
+        a_cur = a_next;
+    }
+    named_bar(4, NT);
+    if (a_prev) axpy(HC, bcB);
+}
+
+template <int S, int R, int C>
+__device__ __forceinline__ void ws_reducer_early(Pipe<S>& pp, const double* __restrict__ cols,
+                                                 const double* __restrict__ a, idx_t p0, int cnt,
+                                                 int m, const double* redA, const double* redB,
+                                                 double* bcA, double* bcB) {
+    constexpr int HC = C / 2, NT = kWsThreads, NW = kWsT / 32;
+    static_assert(S >= 3, "stages j, j+1, j+2 live at once");
+    const int rt = threadIdx.x - kWsT;  // 0..127
+    const int w = rt >> 5, lane = rt & 31;
+    const bool producer = rt == 0;
+    const double* sd = pp.sd;
+    const double* sden = pp.sden;
+    const double* sy = pp.sy;
+    auto wait_stage = [&](int j) {
+        if (producer) mbar_wait_a(pp.full_a + 8 * (j % S), (j / S) & 1u);
+    };
+    auto reduce = [&](const double* red, double* bc, double denom, double y) {
+        for (int c = w; c < HC; c += 4) {
+            double q[NW];
+#pragma unroll
+            for (int k = 0; k < NW; ++k) q[k] = red[c * kWsT + lane + 32 * k];
+            const double v = warp_butterfly32(lane_tree<NW>(q));
+            const double g = PDAS_HOIST_WS ? div_by(v, denom, y) : v / denom;
+            if (lane == 0) bc[c] = g;
+        }
+    };
+    if (producer)
+        for (int i = 0; i < (cnt < S ? cnt : S); ++i)
+            pipe_issue(pp, i, cols + (p0 + i) * m, a + (p0 + i) * m, m, false);
+    wait_stage(0);
+    if (cnt > 1) wait_stage(1);
+    named_arrive(3, NT);
+    bool act = sd[0] != 1.0;
+    double den = sden[0], y = sy[0];
+    for (int j = 0; j < cnt; ++j) {
+        const int jn = j + 1 < cnt ? j + 1 : j;
+        const bool act_n = sd[jn] != 1.0;
+        const double den_n = sden[jn], y_n = sy[jn];
+        // ---- R1(j)
+        WS_MARK(1, j, 0);
+        named_bar(1, NT);  // partials A(j) published
+        WS_MARK(1, j, 1);
+        if (act) reduce(redA, bcA, den, y);
+        WS_MARK(1, j, 2);
+        named_arrive(3, NT);
+        WS_MARK(1, j, 3);
+        // ---- R2(j)
+        named_bar(2, NT);  // partials B(j) published; stage j fully read
+        WS_MARK(1, j, 4);
+        if (act) reduce(redB, bcB, den, y);
+        if (j + 2 < cnt) wait_stage(j + 2);  // C1(j+1) reads A_{j+2}
+        named_arrive(4, NT);
+        WS_MARK(1, j, 5);
+        if (producer && j + S < cnt)
+            pipe_issue(pp, j + S, cols + (p0 + j + S) * m, a + (p0 + j + S) * m, m, false);
+        act = act_n;
+        den = den_n;
+        y = y_n;
+    }
+    named_bar(1, NT);  // the compute warps' final PA arrival
 }
 
 template <int S, int R, int C>
@@ -633,16 +854,17 @@ __device__ __forceinline__ void ws_reducer(Pipe<S>& pp, const double* __restrict
     const bool producer = rt == 0;
     const double* sd = pp.sd;
     const double* sden = pp.sden;
+    const double* sy = pp.sy;
     auto wait_stage = [&](int j) {
         if (producer) mbar_wait_a(pp.full_a + 8 * (j % S), (j / S) & 1u);
     };
-    auto reduce = [&](const double* red, double* bc, double denom) {
+    auto reduce = [&](const double* red, double* bc, double denom, double y) {
         for (int c = w; c < HC; c += 4) {
             double q[NW];
 #pragma unroll
             for (int k = 0; k < NW; ++k) q[k] = red[c * kWsT + lane + 32 * k];
             const double v = warp_butterfly32(lane_tree<NW>(q));
-            const double g = v / denom;
+            const double g = PDAS_HOIST_WS ? div_by(v, denom, y) : v / denom;
             if (lane == 0) bc[c] = g;
         }
     };
@@ -653,19 +875,38 @@ __device__ __forceinline__ void ws_reducer(Pipe<S>& pp, const double* __restrict
             pipe_issue(pp, i, cols + (p0 + i) * m, a + (p0 + i) * m, m, false);
     wait_stage(0);
     named_arrive(3, NT);
+    // pivot scalars are read one step ahead, off the barrier -> reduce chain
+    bool act = sd[0] != 1.0;
+    double den = sden[0], y = sy[0];
     for (int j = 0; j < cnt; ++j) {
+        const int jn = j + 1 < cnt ? j + 1 : j;
+        const bool act_n = sd[jn] != 1.0;
+        const double den_n = sden[jn], y_n = sy[jn];
         // ---- R1(j)
+        WS_MARK(1, j, 0);
         named_bar(1, NT);  // partials A(j) published (C2(j-1) done: stage j-1 free)
-        if (j >= 1 && producer && j - 1 + S < cnt)
+        WS_MARK(1, j, 1);
+        if (!PDAS_ISSUE_LATE && j >= 1 && producer && j - 1 + S < cnt)
             pipe_issue(pp, j - 1 + S, cols + (p0 + j - 1 + S) * m, a + (p0 + j - 1 + S) * m, m,
                        false);
-        if (sd[j] != 1.0) reduce(redA, bcA, sden[j]);
+        if (act) reduce(redA, bcA, den, y);
+        WS_MARK(1, j, 2);
         if (j + 1 < cnt) wait_stage(j + 1);
         named_arrive(3, NT);
+        WS_MARK(1, j, 3);
+        // refill the stage C2(j-1) released, after gA(j) is out
+        if (PDAS_ISSUE_LATE && j >= 1 && producer && j - 1 + S < cnt)
+            pipe_issue(pp, j - 1 + S, cols + (p0 + j - 1 + S) * m, a + (p0 + j - 1 + S) * m, m,
+                       false);
         // ---- R2(j)
         named_bar(2, NT);  // partials B(j) published
-        if (sd[j] != 1.0) reduce(redB, bcB, sden[j]);
+        WS_MARK(1, j, 4);
+        if (act) reduce(redB, bcB, den, y);
         named_arrive(4, NT);
+        WS_MARK(1, j, 5);
+        act = act_n;
+        den = den_n;
+        y = y_n;
     }
     named_bar(1, NT);  // the compute warps' final PA arrival
 }
@@ -696,7 +937,10 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     double* bcB = bc + HC;
     if (threadIdx.x >= kWsT) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kWsRegsReducer));
-        ws_reducer<S, R, C>(pp, cols, a, p0, cnt, m, redA, redB, bcA, bcB);
+        if constexpr (PDAS_WS_EARLY && S >= 3 && R <= 4)
+            ws_reducer_early<S, R, C>(pp, cols, a, p0, cnt, m, redA, redB, bcA, bcB);
+        else
+            ws_reducer<S, R, C>(pp, cols, a, p0, cnt, m, redA, redB, bcA, bcB);
         return;
     }
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kWsRegsCompute));
@@ -704,10 +948,18 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     tl.init(threadIdx.x, m, 0, red, bc);
     const idx_t col0 = (tiles ? tiles[blockIdx.x] : tile0 + blockIdx.x) * C;
     tl.load(cols, col0, n + 1);
-    if (__all_sync(0xffffffffu, tl.full()))
-        ws_compute<S, R, C, true>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
-    else
-        ws_compute<S, R, C, false>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
+    const bool full = __all_sync(0xffffffffu, tl.full());
+    if constexpr (PDAS_WS_EARLY && S >= 3 && R <= 4) {
+        if (full)
+            ws_compute_early<S, R, C, true>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
+        else
+            ws_compute_early<S, R, C, false>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
+    } else {
+        if (full)
+            ws_compute<S, R, C, true>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
+        else
+            ws_compute<S, R, C, false>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
+    }
     tl.store(cols, col0, n + 1);
 }
 
@@ -782,8 +1034,11 @@ __global__ void __launch_bounds__(T, 1)
             break;
         }
         const idx_t e = tp * C + C < p1 ? tp * C + C : p1;
-        if (threadIdx.x < C && tp * C + threadIdx.x < e)
-            pp.sden[tp * C + threadIdx.x - q0] = __ldcg(denoms + tp * C + threadIdx.x);
+        if (threadIdx.x < C && tp * C + threadIdx.x < e) {
+            const double den = __ldcg(denoms + tp * C + threadIdx.x);
+            pp.sden[tp * C + threadIdx.x - q0] = den;
+            pp.sy[tp * C + threadIdx.x - q0] = div_recip(den);
+        }
         fence_proxy_async_global();  // peer CTA's generic stores -> our TMA reads
         __syncthreads();
         apply_global<TMA>(tl, pp, cols, a, q0, tp * C, e, producer);
@@ -825,13 +1080,14 @@ __global__ void __launch_bounds__(T, 1)
                 }
                 if (active) {
                     double inner[C];
-                    tl.template finish<false>(part, 0.0, inner);
+                    tl.template finish<false>(part, 0.0, 0.0, inner);
                     const double denom = 1.0 + inner[cl];
                     if (fabs(denom) <= kDenomEpsRel * (1.0 + fabs(inner[cl]))) {
                         if (producer) *fail = (int32_t)(l + 1);
                         broken = true;
                     } else {
                         if (producer) denoms[l] = denom;
+                        const double yd = div_recip(denom);
                         double pl[R], ph[R];
 #pragma unroll
                         for (int r = 0; r < R; ++r) {
@@ -840,7 +1096,7 @@ __global__ void __launch_bounds__(T, 1)
                         }
 #pragma unroll
                         for (int c = cl + 1; c < C; ++c) {
-                            const double g = inner[c] / denom;
+                            const double g = PDAS_HOIST_TRI ? div_by(inner[c], denom, yd) : inner[c] / denom;
 #pragma unroll
                             for (int r = 0; r < R; ++r) {
                                 if (tl.vlo(r)) {
@@ -1030,6 +1286,17 @@ static int run_cascade(double* cols, const double* a, const double* d, int m, id
 }
 
 idx_t cascade_flags_count(idx_t m, idx_t n) { return n + 2; }
+
+#if PDAS_WS_TRACE
+}  // namespace pdas
+extern "C" int pdas_debug_ws_trace(long long* host_out) {
+    return cudaMemcpyFromSymbol(host_out, pdas::g_ws_trace, sizeof(pdas::g_ws_trace)) ==
+                   cudaSuccess
+               ? 0
+               : -2;
+}
+namespace pdas {
+#endif
 
 int cascade_tile_width(idx_t m) { return cascade_cfg(m).CT; }
 

@@ -50,6 +50,8 @@ int launch_dot3(const double* u0, const double* v0, idx_t l0, double* o0, const 
                 idx_t l2, double* o2, cudaStream_t st);
 
 int launch_fp64_probe(double* sink, idx_t iters, idx_t* ops, cudaStream_t st);
+int launch_div_selftest(const double* a, const double* b, idx_t n, double* fast, double* ref,
+                        cudaStream_t st);
 
 // factor_kernels.cu
 int launch_gram(const double* a, idx_t m, idx_t n, const double* d, double* g, cudaStream_t st);

@@ -518,4 +518,25 @@ int launch_fp64_probe(double* sink, idx_t iters, idx_t* ops, cudaStream_t st) {
     *ops = (idx_t)blocks * 256 * iters * 16;
     return PDAS_OK;
 }
+
+// div_by (hoisted-reciprocal division, common.cuh) against the plain IEEE
+// division on the same operands: out_fast[i] = div_by(a, b, div_recip(b)),
+// out_ref[i] = a / b.
+__global__ void k_div_selftest(const double* __restrict__ a, const double* __restrict__ b,
+                               idx_t n, double* __restrict__ fast, double* __restrict__ ref) {
+    for (idx_t i = blockIdx.x * (idx_t)blockDim.x + threadIdx.x; i < n;
+         i += (idx_t)gridDim.x * blockDim.x) {
+        const double x = a[i], y = b[i];
+        fast[i] = div_by(x, y, div_recip(y));
+        ref[i] = x / y;
+    }
+}
+
+int launch_div_selftest(const double* a, const double* b, idx_t n, double* fast, double* ref,
+                        cudaStream_t st) {
+    if (n <= 0) return PDAS_OK;
+    const idx_t blocks = (n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16;
+    k_div_selftest<<<(unsigned)blocks, 256, 0, st>>>(a, b, n, fast, ref);
+    return PDAS_OK;
+}
 }  // namespace pdas
