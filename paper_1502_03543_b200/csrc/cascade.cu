@@ -36,6 +36,9 @@
 #include "pdas_internal.h"
 #include "tma.cuh"
 
+#ifndef PDAS_CASC_EARLYPANEL
+#define PDAS_CASC_EARLYPANEL 1
+#endif
 #ifndef PDAS_HOIST_WS
 #define PDAS_HOIST_WS 0
 #endif
@@ -643,6 +646,10 @@ __device__ __forceinline__ void ws_compute(Tile<kWsT, R, C, false>& tl, const do
         partials(0, redA);
     }
     named_arrive(1, NT);
+    // stage pointers of pivots j and j+1, advanced incrementally (no j % S)
+    const double* const ring_end = buf + S * stage;
+    const double* st_cur = buf;
+    const double* st_nxt = S > 1 ? buf + stage : buf;
     for (int j = 0; j < cnt; ++j) {
 #if PDAS_PREFETCH_ACT
         // d of pivot j+1, read before the barriers it would otherwise follow
@@ -667,17 +674,19 @@ __device__ __forceinline__ void ws_compute(Tile<kWsT, R, C, false>& tl, const do
         const bool a_next = j + 1 < cnt && dn != 1.0;
 #endif
         if (a_cur) {
-            tl.template load_p<false, FULL>(sptr(j), pl, ph);
+            tl.template load_p<false, FULL>(st_cur, pl, ph);
             axpy(0, bcA);
         }
         if (a_next) {
-            tl.template make_v<false, FULL>(sptr(j + 1) + mp, dn - 1.0, vl, vh);
+            tl.template make_v<false, FULL>(st_nxt + mp, dn - 1.0, vl, vh);
             partials(0, redA);
         }
         named_arrive(1, NT);
         WS_MARK(0, j, 4);
         a_prev = a_cur;
         a_cur = a_next;
+        st_cur = st_nxt;
+        st_nxt = st_nxt + stage == ring_end ? buf : st_nxt + stage;
     }
     named_bar(4, NT);
     if (a_prev) axpy(HC, bcB);
@@ -875,6 +884,7 @@ __device__ __forceinline__ void ws_reducer(Pipe<S>& pp, const double* __restrict
             pipe_issue(pp, i, cols + (p0 + i) * m, a + (p0 + i) * m, m, false);
     wait_stage(0);
     named_arrive(3, NT);
+    uint32_t w_slot = 1u % S, w_par = (1u / S) & 1u;  // stage/parity of pivot j+1
     // pivot scalars are read one step ahead, off the barrier -> reduce chain
     bool act = sd[0] != 1.0;
     double den = sden[0], y = sy[0];
@@ -891,7 +901,11 @@ __device__ __forceinline__ void ws_reducer(Pipe<S>& pp, const double* __restrict
                        false);
         if (act) reduce(redA, bcA, den, y);
         WS_MARK(1, j, 2);
-        if (j + 1 < cnt) wait_stage(j + 1);
+        if (j + 1 < cnt && producer) mbar_wait_a(pp.full_a + 8 * w_slot, w_par);
+        if (++w_slot == (uint32_t)S) {
+            w_slot = 0;
+            w_par ^= 1u;
+        }
         named_arrive(3, NT);
         WS_MARK(1, j, 3);
         // refill the stage C2(j-1) released, after gA(j) is out
@@ -918,7 +932,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     k_casc_update_ws(double* __restrict__ cols, const double* __restrict__ a,
                      const double* __restrict__ d, const double* __restrict__ denoms, int m,
                      idx_t n, idx_t p0, idx_t p1, idx_t tile0, const int32_t* __restrict__ fail,
-                     const int64_t* __restrict__ tiles) {
+                     const int64_t* __restrict__ tiles, int* __restrict__ uflag, int utag,
+                     int ucount) {
     if (*(volatile const int32_t*)fail) return;
     double *red, *bc;
     Pipe<S> pp;
@@ -961,6 +976,11 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             ws_compute<S, R, C, false>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
     }
     tl.store(cols, col0, n + 1);
+    if (uflag && (int)blockIdx.x < ucount) {  // tile done: the next panel may take it
+        __threadfence();
+        named_bar(5, kWsT);
+        if (threadIdx.x == 0) st_release(uflag + col0 / C, utag);
+    }
 }
 
 // ------------------------------------------------------------ update kernel
@@ -971,7 +991,8 @@ __global__ void __launch_bounds__(T* G, 1)
     k_casc_update(double* __restrict__ cols, const double* __restrict__ a,
                   const double* __restrict__ d, const double* __restrict__ denoms, int m, idx_t n,
                   idx_t p0, idx_t p1, idx_t tile0, const int32_t* __restrict__ fail,
-                  const int64_t* __restrict__ tiles) {
+                  const int64_t* __restrict__ tiles, int* __restrict__ uflag, int utag,
+                     int ucount) {
     if (*(volatile const int32_t*)fail) return;
     double *red, *bc;
     Pipe<S> pp;
@@ -981,7 +1002,8 @@ __global__ void __launch_bounds__(T* G, 1)
     const int grp = threadIdx.x / T;
     Tile<T, R, C, GEN> tl;
     tl.init(threadIdx.x % T, m, 1 + grp, red + grp * C * T, bc + grp * C);
-    const idx_t col0 = (tiles ? tiles[blockIdx.x] : tile0 + blockIdx.x) * (C * G) + grp * C;
+    const idx_t tile = tiles ? tiles[blockIdx.x] : tile0 + blockIdx.x;
+    const idx_t col0 = tile * (C * G) + grp * C;
     tl.load(cols, col0, n + 1);
     if constexpr (TMA && G == 2 && !GEN && S >= 4) {
         const int cnt = (int)(p1 - p0);
@@ -996,6 +1018,11 @@ __global__ void __launch_bounds__(T* G, 1)
         apply_global<TMA>(tl, pp, cols, a, p0, p0, p1, threadIdx.x == 0);
     }
     tl.store(cols, col0, n + 1);
+    if (uflag && (int)blockIdx.x < ucount) {
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) st_release(uflag + tile, utag);
+    }
 }
 
 // ------------------------------------------------------------ panel kernel
@@ -1008,8 +1035,12 @@ __global__ void __launch_bounds__(T, 1)
     k_casc_panel(double* __restrict__ cols, const double* __restrict__ a,
                  const double* __restrict__ d, double* __restrict__ denoms, int m, idx_t n,
                  idx_t q0, idx_t p0, idx_t p1, int32_t* __restrict__ fail, int* __restrict__ flags,
-                 int epoch) {
-    if (*(volatile int32_t*)fail) return;
+                 int epoch, const int* __restrict__ uflag, int utag) {
+    const idx_t tile = p0 / C + blockIdx.x;
+    if (*(volatile int32_t*)fail) {  // still publish: later tiles may be waiting
+        if (threadIdx.x == 0) st_release(flags + tile, epoch);
+        return;
+    }
     double *red, *bc;
     Pipe<S> pp;
     carve<T, C, 1, S>(red, bc, pp, TMA, m);
@@ -1020,12 +1051,24 @@ __global__ void __launch_bounds__(T, 1)
     Tile<T, R, C, GEN> tl;
     tl.init(threadIdx.x, m, 1, red, bc);
     const bool producer = threadIdx.x == 0;
-    const idx_t tile = p0 / C + blockIdx.x;
     const idx_t col0 = tile * C;
-    tl.load(cols, col0, n + 1);
-    apply_global<TMA>(tl, pp, cols, a, q0, q0, p0, producer);
     bool dead = false;
-    for (idx_t tp = p0 / C; tp < tile; ++tp) {
+    if (uflag) {
+        // this tile's last update (the update kernel of the previous block,
+        // running concurrently) must have landed before the tile is read
+        if (producer)
+            while (ld_acquire(uflag + tile) != utag) {
+                if (*(volatile int32_t*)fail) break;
+                __nanosleep(64);
+            }
+        __syncthreads();
+        dead = *(volatile int32_t*)fail != 0;
+    }
+    if (!dead) {
+        tl.load(cols, col0, n + 1);
+        apply_global<TMA>(tl, pp, cols, a, q0, q0, p0, producer);
+    }
+    for (idx_t tp = p0 / C; tp < tile && !dead; ++tp) {
         if (producer)
             while (ld_acquire(flags + tp) != epoch) __nanosleep(32);
         __syncthreads();
@@ -1210,7 +1253,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
     if (op.kind == 1) {
         if (op.p0 % CT || op.p1 <= op.p0 || op.p1 - op.q0 > 2 * kMaxBlock) return PDAS_ERR_ARG;
         kp<<<(unsigned)((op.p1 - op.p0 + CT - 1) / CT), T, smem_p, st>>>(
-            cols, a, d, denoms, m, n, op.q0, op.p0, op.p1, fail, flags, epoch);
+            cols, a, d, denoms, m, n, op.q0, op.p0, op.p1, fail, flags, epoch, nullptr, 0);
         return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
     }
     if (op.kind == 2) {
@@ -1218,43 +1261,79 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         if (op.ntiles > 0) {
             if (use_ws)
                 kws<<<(unsigned)op.ntiles, kWsThreads, smem_ws, st>>>(
-                    cols, a, d, denoms, m, n, op.p0, op.p1, 0, fail, op.tiles);
+                    cols, a, d, denoms, m, n, op.p0, op.p1, 0, fail, op.tiles, nullptr, 0, 0);
             else
                 ku<<<(unsigned)op.ntiles, T * G, smem_u, st>>>(cols, a, d, denoms, m, n, op.p0,
-                                                               op.p1, 0, fail, op.tiles);
+                                                               op.p1, 0, fail, op.tiles, nullptr, 0, 0);
         }
         return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
     }
     const idx_t nb = (n + B - 1) / B;
     auto blk_end = [&](idx_t b) { return (b + 1) * B < n ? (b + 1) * B : n; };
     auto tiles_of = [&](idx_t b) { return (blk_end(b) - b * B + CT - 1) / CT; };
+    auto update = [&](idx_t b, idx_t t0, int* uf) {
+        if (t0 >= ntiles) return;
+        const int uc = uf && b + 1 < nb ? (int)tiles_of(b + 1) : 0;
+        if (use_ws)
+            kws<<<(unsigned)(ntiles - t0), kWsThreads, smem_ws, st>>>(
+                cols, a, d, denoms, m, n, b * B, blk_end(b), t0, fail, nullptr, uf, (int)(b + 1), uc);
+        else
+            ku<<<(unsigned)(ntiles - t0), T * G, smem_u, st>>>(
+                cols, a, d, denoms, m, n, b * B, blk_end(b), t0, fail, nullptr, uf, (int)(b + 1), uc);
+    };
     SideStream& ss = side_stream();
+    if (PDAS_CASC_EARLYPANEL) {
+        // U(b) covers block b+1's tiles too (its lowest CTAs) and flags each
+        // tile as it lands; panel(b+1) -- only the block's own chain and
+        // triangle -- waits on those flags inside the kernel, so it starts as
+        // soon as its 16-odd tiles are done instead of after all of U(b).
+        int* uflag = flags + (n + 2);
+        cudaMemsetAsync(uflag, 0, sizeof(int) * (size_t)(n + 2), st);
+        cudaEventRecord(ss.e0, st);
+        cudaStreamWaitEvent(ss.ps, ss.e0, 0);
+        kp<<<(unsigned)tiles_of(0), T, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, 0, 0,
+                                                        blk_end(0), fail, flags, epoch, nullptr, 0);
+        cudaEventRecord(ss.eP, ss.ps);
+        for (idx_t b = 0; b < nb; ++b) {
+            cudaStreamWaitEvent(st, ss.eP, 0);  // panel(b): block b is final
+            // eU marks the START of U(b): panel(b+1) must not be resident (and
+            // spinning on 16-odd SMs) while U(b-1) still runs
+            cudaEventRecord(ss.eU, st);
+            const idx_t t0 = b + 1 < nb ? (b + 1) * B / CT : (n + CT - 1) / CT;
+            update(b, t0, uflag);
+            if (b + 1 < nb) {
+                const idx_t p0 = (b + 1) * B;
+                cudaStreamWaitEvent(ss.ps, ss.eU, 0);
+                kp<<<(unsigned)tiles_of(b + 1), T, smem_p, ss.ps>>>(
+                    cols, a, d, denoms, m, n, p0, p0, blk_end(b + 1), fail, flags, epoch, uflag,
+                    (int)(b + 1));
+                cudaEventRecord(ss.eP, ss.ps);
+            }
+        }
+        // join: the caller's stream sees every panel
+        cudaEventRecord(ss.eP, ss.ps);
+        cudaStreamWaitEvent(st, ss.eP, 0);
+        return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
+    }
     cudaEventRecord(ss.e0, st);
     cudaStreamWaitEvent(ss.ps, ss.e0, 0);
     cudaEventRecord(ss.eU, st);
     kp<<<(unsigned)tiles_of(0), T, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, 0, 0, blk_end(0),
-                                                    fail, flags, epoch);
+                                                    fail, flags, epoch, nullptr, 0);
     cudaEventRecord(ss.eP, ss.ps);
     for (idx_t b = 0; b < nb; ++b) {
         cudaStreamWaitEvent(st, ss.eP, 0);  // panel(b): block b is final
         if (b + 1 < nb) {
             // panel(b+1) needs block b (stream order on ps) and U_rest(b-1)
             cudaStreamWaitEvent(ss.ps, ss.eU, 0);
-            kp<<<(unsigned)tiles_of(b + 1), T, smem_p, ss.ps>>>(
-                cols, a, d, denoms, m, n, b * B, (b + 1) * B, blk_end(b + 1), fail, flags, epoch);
+            kp<<<(unsigned)tiles_of(b + 1), T, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, b * B,
+                                                                (b + 1) * B, blk_end(b + 1), fail,
+                                                                flags, epoch, nullptr, 0);
             cudaEventRecord(ss.eP, ss.ps);
         }
         // U_rest(b): every tile beyond block b+1 (or beyond block b at the end)
         const idx_t last = b + 1 < nb ? blk_end(b + 1) : blk_end(b);
-        const idx_t t0 = (last + CT - 1) / CT;
-        if (t0 < ntiles) {
-            if (use_ws)
-                kws<<<(unsigned)(ntiles - t0), kWsThreads, smem_ws, st>>>(
-                    cols, a, d, denoms, m, n, b * B, blk_end(b), t0, fail, nullptr);
-            else
-                ku<<<(unsigned)(ntiles - t0), T * G, smem_u, st>>>(cols, a, d, denoms, m, n, b * B,
-                                                                   blk_end(b), t0, fail, nullptr);
-        }
+        update(b, (last + CT - 1) / CT, nullptr);
         cudaEventRecord(ss.eU, st);
     }
     return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
@@ -1266,7 +1345,11 @@ static int run_cascade(double* cols, const double* a, const double* d, int m, id
                        cudaStream_t st, const CascOp& op) {
     B = (B + CT - 1) / CT * CT;
     if (B > kMaxBlock) B = kMaxBlock / CT * CT;
-    const bool aligned = (m % 2 == 0) && (((uintptr_t)cols | (uintptr_t)a) % 16 == 0);
+    // TMA pivot staging pays off only for the 256-thread tiles (m > 256); for
+    // smaller m the per-pivot bulk-copy + mbarrier round trip dominates the
+    // step (measured 3-5x slower than direct L2 loads at m = 50 / 64).
+    const bool aligned = T == 256 && (m % 2 == 0) &&
+                         (((uintptr_t)cols | (uintptr_t)a) % 16 == 0);
     const size_t budget = 210 * 1024;
     if (aligned && env_int("PDAS_CASCADE_STAGES", 5) >= 5 &&
         casc_smem_bytes<T, CT, 1>(5, m) <= budget &&
@@ -1285,7 +1368,7 @@ static int run_cascade(double* cols, const double* a, const double* d, int m, id
                                                        epoch, B, st, op);
 }
 
-idx_t cascade_flags_count(idx_t m, idx_t n) { return n + 2; }
+idx_t cascade_flags_count(idx_t m, idx_t n) { return 2 * (n + 2); }  // panel + update flags
 
 #if PDAS_WS_TRACE
 }  // namespace pdas
