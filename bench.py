@@ -356,8 +356,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-sample-steps", type=int, default=200)
-    ap.add_argument("--ref-sample-steps", type=int, default=200)
+    ap.add_argument("--cpu-sample-steps", type=int, default=1500)
+    ap.add_argument("--ref-sample-steps", type=int, default=1500)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--mode", default="shard", choices=["shard", "replicas"],
                     help="N>1: one LP column-sharded over the GPUs, or N independent LPs")

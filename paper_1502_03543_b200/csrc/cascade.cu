@@ -568,12 +568,18 @@ __device__ __forceinline__ void apply_global(Tile<T, R, C, GEN>& tl, Pipe<S>& pp
 #ifndef PDAS_PREFETCH_ACT
 #define PDAS_PREFETCH_ACT 1
 #endif
+#ifndef PDAS_WS_LDG
+#define PDAS_WS_LDG 1
+#endif
 #ifndef PDAS_WS_EARLY
 #define PDAS_WS_EARLY 0
 #endif
 constexpr int kWsT = 256;       // compute threads
 constexpr int kWsThreads = 384; // + reducer warpgroup
-constexpr int kWsRegsCompute = 232, kWsRegsReducer = 40;
+#ifndef PDAS_WS_REGS_R
+#define PDAS_WS_REGS_R 40
+#endif
+constexpr int kWsRegsCompute = 232, kWsRegsReducer = PDAS_WS_REGS_R;
 
 // Diagnostic build only (make variant VDEFS=-DPDAS_WS_TRACE=1): clock64 marks
 // of compute thread 0 / reducer thread 0 of one CTA per pivot, read back with
@@ -852,6 +858,153 @@ __device__ __forceinline__ void ws_reducer_early(Pipe<S>& pp, const double* __re
     named_bar(1, NT);  // the compute warps' final PA arrival
 }
 
+// Direct-load variant: P_l and A[:,l] go L2 -> registers (ld.global.cg), one
+// pivot ahead, instead of through a TMA ring in shared memory.  Shared-memory
+// traffic per pivot drops from ~100 KB (TMA writes + stage reads +
+// reductions) to the 32 KB of the reductions; the reducer warpgroup only
+// reduces.  Same arithmetic, same order.
+template <int R, int C, bool FULL>
+__device__ __forceinline__ void ws_compute_ldg(Tile<kWsT, R, C, false>& tl,
+                                               const double* __restrict__ pcol,
+                                               const double* __restrict__ acol, int m,
+                                               const double* sd, int cnt, double* redA,
+                                               double* redB, const double* bcA,
+                                               const double* bcB) {
+    constexpr int HC = C / 2, NT = kWsThreads;
+    double vl[R], vh[R], pl[R], ph[R];
+    double npl[R], nph[R], nal[R], nah[R];  // P_{j+1}, raw A_{j+2} in flight
+    auto partials = [&](int h0, double* red) {
+#pragma unroll
+        for (int c = 0; c < HC; ++c) {
+            double s[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                double lo = vl[r] * tl.xl[r][h0 + c];
+                double hi = vh[r] * tl.xh[r][h0 + c];
+                s[r] = lo + hi;
+            }
+            red[c * kWsT + tl.t] = lane_tree<R>(s);
+        }
+    };
+    auto axpy = [&](int h0, const double* bc) {
+        double g[HC];
+#pragma unroll
+        for (int c = 0; c < HC; ++c) g[c] = bc[c];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const bool hi = FULL || tl.vhi(r);
+#pragma unroll
+            for (int c = 0; c < HC; ++c) {
+                double q0 = g[c] * pl[r];
+                tl.xl[r][h0 + c] = tl.xl[r][h0 + c] - q0;
+            }
+            if (hi) {
+#pragma unroll
+                for (int c = 0; c < HC; ++c) {
+                    double q1 = g[c] * ph[r];
+                    tl.xh[r][h0 + c] = tl.xh[r][h0 + c] - q1;
+                }
+            }
+        }
+    };
+    auto scale = [&](double f) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            vl[r] = nal[r] * f;
+            vh[r] = (FULL || tl.vhi(r)) ? nah[r] * f : 0.0;
+        }
+    };
+    // prologue: v_0, P_0 and A_1 in registers / in flight
+    tl.template load_p<true, FULL>(acol, nal, nah);
+    tl.template load_p<true, FULL>(pcol, npl, nph);
+    bool a_prev = false, a_cur = sd[0] != 1.0;
+    scale(sd[0] - 1.0);
+    if (cnt > 1) tl.template load_p<true, FULL>(acol + m, nal, nah);
+    if (a_cur) partials(0, redA);
+    named_arrive(1, NT);
+#ifndef PDAS_WS_UNROLL2
+#define PDAS_WS_UNROLL2 1
+#endif
+#if PDAS_WS_UNROLL2
+#pragma unroll 2
+#endif
+    for (int j = 0; j < cnt; ++j) {
+        const double dn = sd[j + 1 < cnt ? j + 1 : j];
+        const bool a_next = j + 1 < cnt && dn != 1.0;
+        // ---- C1(j)
+        WS_MARK(0, j, 0);
+        if (j > 0) {
+            named_bar(4, NT);
+            WS_MARK(0, j, 1);
+            if (a_prev) axpy(HC, bcB);
+        }
+        if (a_cur) partials(HC, redB);
+        named_arrive(2, NT);
+        WS_MARK(0, j, 2);
+        // ---- C2(j)
+        named_bar(3, NT);  // gA(j) ready
+        WS_MARK(0, j, 3);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            pl[r] = npl[r];
+            ph[r] = nph[r];
+        }
+        if (j + 1 < cnt) tl.template load_p<true, FULL>(pcol + (size_t)(j + 1) * m, npl, nph);
+        if (a_cur) axpy(0, bcA);
+        scale(dn - 1.0);
+        if (j + 2 < cnt) tl.template load_p<true, FULL>(acol + (size_t)(j + 2) * m, nal, nah);
+        if (a_next) partials(0, redA);
+        named_arrive(1, NT);
+        WS_MARK(0, j, 4);
+        a_prev = a_cur;
+        a_cur = a_next;
+    }
+    named_bar(4, NT);
+    if (a_prev) axpy(HC, bcB);
+}
+
+template <int R, int C>
+__device__ __forceinline__ void ws_reducer_ldg(const double* sd, const double* sden,
+                                               const double* sy, int cnt, const double* redA,
+                                               const double* redB, double* bcA, double* bcB) {
+    constexpr int HC = C / 2, NT = kWsThreads, NW = kWsT / 32;
+    const int rt = threadIdx.x - kWsT;  // 0..127
+    const int w = rt >> 5, lane = rt & 31;
+    auto reduce = [&](const double* red, double* bc, double denom, double y) {
+        for (int c = w; c < HC; c += 4) {
+            double q[NW];
+#pragma unroll
+            for (int k = 0; k < NW; ++k) q[k] = red[c * kWsT + lane + 32 * k];
+            const double v = warp_butterfly32(lane_tree<NW>(q));
+            const double g = PDAS_HOIST_WS ? div_by(v, denom, y) : v / denom;
+            if (lane == 0) bc[c] = g;
+        }
+    };
+    bool act = sd[0] != 1.0;
+    double den = sden[0], y = sy[0];
+    for (int j = 0; j < cnt; ++j) {
+        const int jn = j + 1 < cnt ? j + 1 : j;
+        const bool act_n = sd[jn] != 1.0;
+        const double den_n = sden[jn], y_n = sy[jn];
+        WS_MARK(1, j, 0);
+        named_bar(1, NT);  // partials A(j) published
+        WS_MARK(1, j, 1);
+        if (act) reduce(redA, bcA, den, y);
+        WS_MARK(1, j, 2);
+        named_arrive(3, NT);
+        WS_MARK(1, j, 3);
+        named_bar(2, NT);  // partials B(j) published
+        WS_MARK(1, j, 4);
+        if (act) reduce(redB, bcB, den, y);
+        named_arrive(4, NT);
+        WS_MARK(1, j, 5);
+        act = act_n;
+        den = den_n;
+        y = y_n;
+    }
+    named_bar(1, NT);  // the compute warps' final PA arrival
+}
+
 template <int S, int R, int C>
 __device__ __forceinline__ void ws_reducer(Pipe<S>& pp, const double* __restrict__ cols,
                                            const double* __restrict__ a, idx_t p0, int cnt, int m,
@@ -938,7 +1091,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     double *red, *bc;
     Pipe<S> pp;
     carve<kWsT, C, 1, S>(red, bc, pp, false, m);
-    if (threadIdx.x == 0) {
+    if (!(PDAS_WS_LDG && R <= 4) && threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) mbar_init(pp.full + s, 1);
         mbar_fence_init();
     }
@@ -952,7 +1105,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     double* bcB = bc + HC;
     if (threadIdx.x >= kWsT) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kWsRegsReducer));
-        if constexpr (PDAS_WS_EARLY && S >= 3 && R <= 4)
+        if constexpr (PDAS_WS_LDG && R <= 4)
+            ws_reducer_ldg<R, C>(pp.sd, pp.sden, pp.sy, cnt, redA, redB, bcA, bcB);
+        else if constexpr (PDAS_WS_EARLY && S >= 3 && R <= 4)
             ws_reducer_early<S, R, C>(pp, cols, a, p0, cnt, m, redA, redB, bcA, bcB);
         else
             ws_reducer<S, R, C>(pp, cols, a, p0, cnt, m, redA, redB, bcA, bcB);
@@ -964,7 +1119,14 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     const idx_t col0 = (tiles ? tiles[blockIdx.x] : tile0 + blockIdx.x) * C;
     tl.load(cols, col0, n + 1);
     const bool full = __all_sync(0xffffffffu, tl.full());
-    if constexpr (PDAS_WS_EARLY && S >= 3 && R <= 4) {
+    if constexpr (PDAS_WS_LDG && R <= 4) {
+        const double* pc = cols + p0 * m;
+        const double* ac = a + p0 * m;
+        if (full)
+            ws_compute_ldg<R, C, true>(tl, pc, ac, m, pp.sd, cnt, redA, redB, bcA, bcB);
+        else
+            ws_compute_ldg<R, C, false>(tl, pc, ac, m, pp.sd, cnt, redA, redB, bcA, bcB);
+    } else if constexpr (PDAS_WS_EARLY && S >= 3 && R <= 4) {
         if (full)
             ws_compute_early<S, R, C, true>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
         else
