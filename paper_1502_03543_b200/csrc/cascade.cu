@@ -191,9 +191,10 @@ struct Tile {
 
     // Per-thread partial (tree levels >= T) of tree(v, column c), all c.
     __device__ __forceinline__ void partials(const double (&vl)[R], const double (&vh)[R],
-                                             double (&part)[C]) const {
+                                             double (&part)[C], int c0 = 0) const {
 #pragma unroll
         for (int c = 0; c < C; ++c) {
+            if (c < c0) continue;
             double s[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -212,10 +213,11 @@ struct Tile {
     }
 
     // First half of the cross-thread reduction: publish partials (T > 32).
-    __device__ __forceinline__ void publish(const double (&part)[C]) const {
+    __device__ __forceinline__ void publish(const double (&part)[C], int c0 = 0) const {
         if (T > 32) {
 #pragma unroll
-            for (int c = 0; c < C; ++c) red[c * T + t] = part[c];
+            for (int c = 0; c < C; ++c)
+                if (c >= c0) red[c * T + t] = part[c];
         }
     }
 
@@ -223,31 +225,49 @@ struct Tile {
     // T/2 .. 1.  DIV: out[c] = inner[c] / denom (one lane per column
     // divides), else out[c] = inner[c].  Ends with the group barrier when
     // T > 32; every thread returns all C values.
+    // c0: only columns >= c0 are reduced (the panel triangle's live columns).
     template <bool DIV>
     __device__ __forceinline__ void finish(const double (&part)[C], double denom, double y,
-                                           double (&out)[C]) const {
+                                           double (&out)[C], int c0 = 0) const {
         const int lane = t & 31;
         if (T == 32) {
             const int w = H >= 32 ? 32 : (H > 0 ? H : 1);
 #pragma unroll
             for (int c = 0; c < C; ++c) {
+                if (c < c0) continue;
                 double v = warp_butterfly(part[c], w);
                 if (GEN && H < 32) v = __shfl_sync(0xffffffffu, v, 0);
                 out[c] = DIV ? (PDAS_HOIST_FIN ? div_by(v, denom, y) : v / denom) : v;
             }
         } else {
             constexpr int NW = T / 32;
+            constexpr int PER = (C + NW - 1) / NW;
             const int warp = t >> 5;
-            for (int c = warp; c < C; c += NW) {
-                double q[NW];
+            // a warp's columns (warp, warp+NW, ...) as independent chains
+            double v[PER];
 #pragma unroll
-                for (int k = 0; k < NW; ++k) q[k] = red[c * T + lane + 32 * k];
-                double v = warp_butterfly32(lane_tree<NW>(q));
-                if (lane == 0) bc[c] = DIV ? (PDAS_HOIST_FIN ? div_by(v, denom, y) : v / denom) : v;
+            for (int k = 0; k < PER; ++k) {
+                const int c = warp + NW * k;
+                if (c >= c0 && c < C) {
+                    double q[NW];
+#pragma unroll
+                    for (int i = 0; i < NW; ++i) q[i] = red[c * T + lane + 32 * i];
+                    v[k] = lane_tree<NW>(q);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int c = warp + NW * k;
+                if (c >= c0 && c < C) {
+                    const double u = warp_butterfly32(v[k]);
+                    if (lane == 0)
+                        bc[c] = DIV ? (PDAS_HOIST_FIN ? div_by(u, denom, y) : u / denom) : u;
+                }
             }
             sync();
 #pragma unroll
-            for (int c = 0; c < C; ++c) out[c] = bc[c];
+            for (int c = 0; c < C; ++c)
+                if (c >= c0) out[c] = bc[c];
         }
     }
 
@@ -341,7 +361,7 @@ __device__ __forceinline__ void pipe_issue(Pipe<S>& p, unsigned use, const doubl
 //               | sy[2*kMaxBlock] | full[S] | empty[S] | stages
 template <int T, int C, int G>
 __host__ __device__ constexpr size_t casc_head_bytes(int S) {
-    return (((size_t)G * C * T + (size_t)G * C + 6 * kMaxBlock + 2 * (size_t)S) * sizeof(double) +
+    return (((size_t)G * C * T + 2 * (size_t)G * C + 6 * kMaxBlock + 2 * (size_t)S) * sizeof(double) +
             127) & ~(size_t)127;
 }
 
@@ -355,8 +375,8 @@ template <int T, int C, int G, int S>
 __device__ __forceinline__ void carve(double*& red, double*& bc, Pipe<S>& pp, bool tma, int m) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     red = reinterpret_cast<double*>(smem_raw);
-    bc = red + G * C * T;
-    pp.sd = bc + G * C;
+    bc = red + G * C * T;  // bc[G*C] (+ G*C scratch: the panel triangle's quotients)
+    pp.sd = bc + 2 * G * C;
     pp.sden = pp.sd + 2 * kMaxBlock;
     pp.sy = pp.sden + 2 * kMaxBlock;
     pp.full = reinterpret_cast<uint64_t*>(pp.sy + 2 * kMaxBlock);
@@ -1274,8 +1294,8 @@ __global__ void __launch_bounds__(T, 1)
                 if (active) {
                     double vl[R], vh[R];
                     tl.template make_v<!TMA, false>(ac, dl - 1.0, vl, vh);
-                    tl.partials(vl, vh, part);
-                    tl.publish(part);
+                    tl.partials(vl, vh, part, cl);  // columns < cl are final
+                    tl.publish(part, cl);
                 }
                 tl.sync();
                 if (TMA && cl > 0) {
@@ -1285,7 +1305,7 @@ __global__ void __launch_bounds__(T, 1)
                 }
                 if (active) {
                     double inner[C];
-                    tl.template finish<false>(part, 0.0, 0.0, inner);
+                    tl.template finish<false>(part, 0.0, 0.0, inner, cl);
                     const double denom = 1.0 + inner[cl];
                     if (fabs(denom) <= kDenomEpsRel * (1.0 + fabs(inner[cl]))) {
                         if (producer) *fail = (int32_t)(l + 1);
@@ -1299,9 +1319,16 @@ __global__ void __launch_bounds__(T, 1)
                             pl[r] = tl.xl[r][cl];
                             ph[r] = tl.xh[r][cl];
                         }
+                        // T > 32: one thread per live column divides, all read the
+                        // quotients back (instead of every thread dividing them all)
+                        if (T > 32 && cl + 1 < C) {
+                            if (threadIdx.x > cl && threadIdx.x < C) bc[C + threadIdx.x] = bc[threadIdx.x] / denom;
+                            tl.sync();
+                        }
 #pragma unroll
                         for (int c = cl + 1; c < C; ++c) {
-                            const double g = PDAS_HOIST_TRI ? div_by(inner[c], denom, yd) : inner[c] / denom;
+                            const double g = T > 32 ? bc[C + c]
+                                             : (PDAS_HOIST_TRI ? div_by(inner[c], denom, yd) : inner[c] / denom);
 #pragma unroll
                             for (int r = 0; r < R; ++r) {
                                 if (tl.vlo(r)) {
