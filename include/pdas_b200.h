@@ -190,6 +190,12 @@ int pdas_probe_fp64(double* sink, int64_t iters, int64_t* ops, void* stream);
 int pdas_selftest_div(const double* a, const double* b, int64_t n, double* out_fast,
                       double* out_ref, void* stream);
 
+/* With PDAS_CASCADE_PROFILE=1 in the environment the 1-GPU cascade records
+ * CUDA events around each update / panel launch (and synchronises at its
+ * end).  Copies the last cascade's rows {kind (0 update, 1 panel), block,
+ * start ms, end ms} (host memory, up to max_rows) and returns the row count. */
+int64_t pdas_debug_cascade_profile(double* out, int64_t max_rows);
+
 #ifdef __cplusplus
 }
 #endif

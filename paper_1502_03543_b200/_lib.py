@@ -86,6 +86,7 @@ SIGNATURES = {
     "pdas_iter_objectives": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _I64, _I64, _VP, _VP]),
     "pdas_probe_fp64": (ctypes.c_int, [_VP, _I64, _VP, _VP]),
     "pdas_selftest_div": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
+    "pdas_debug_cascade_profile": (ctypes.c_int64, [_VP, _I64]),
 }
 
 _LIB = None

@@ -201,6 +201,11 @@ int pdas_cascade_tile_width(int64_t m) {
 
 int pdas_cascade_block_pivots(void) { return pdas::kCascadeBlock; }
 
+int64_t pdas_debug_cascade_profile(double* out, int64_t max_rows) {
+    if (max_rows < 0 || (max_rows > 0 && out == nullptr)) return -1;
+    return pdas::cascade_profile_rows(out, max_rows);
+}
+
 static int split_ws(void* ws, int64_t n, double** denoms, int** flags) {
     const int64_t nd = n > 0 ? n : 1;
     *denoms = static_cast<double*>(ws);

@@ -31,11 +31,15 @@
 //   element-step) becomes the bound.
 #include <climits>
 #include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "pdas_internal.h"
 #include "tma.cuh"
 
+#ifndef PDAS_PANEL_TMA
+#define PDAS_PANEL_TMA 1
+#endif
 #ifndef PDAS_CASC_EARLYPANEL
 #define PDAS_CASC_EARLYPANEL 1
 #endif
@@ -832,14 +836,28 @@ __device__ __forceinline__ void ws_reducer_early(Pipe<S>& pp, const double* __re
     auto wait_stage = [&](int j) {
         if (producer) mbar_wait_a(pp.full_a + 8 * (j % S), (j / S) & 1u);
     };
+    // a warp's columns (w, w+4, ...) as independent chains (HC = 8 at m <= 1024)
     auto reduce = [&](const double* red, double* bc, double denom, double y) {
-        for (int c = w; c < HC; c += 4) {
-            double q[NW];
+        constexpr int PER = (HC + 3) / 4;
+        double v[PER];
 #pragma unroll
-            for (int k = 0; k < NW; ++k) q[k] = red[c * kWsT + lane + 32 * k];
-            const double v = warp_butterfly32(lane_tree<NW>(q));
-            const double g = PDAS_HOIST_WS ? div_by(v, denom, y) : v / denom;
-            if (lane == 0) bc[c] = g;
+        for (int k = 0; k < PER; ++k) {
+            const int c = w + 4 * k;
+            if (c < HC) {
+                double q[NW];
+#pragma unroll
+                for (int i = 0; i < NW; ++i) q[i] = red[c * kWsT + lane + 32 * i];
+                v[k] = lane_tree<NW>(q);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int c = w + 4 * k;
+            if (c < HC) {
+                const double u = warp_butterfly32(v[k]);
+                const double g = PDAS_HOIST_WS ? div_by(u, denom, y) : u / denom;
+                if (lane == 0) bc[c] = g;
+            }
         }
     };
     if (producer)
@@ -990,14 +1008,28 @@ __device__ __forceinline__ void ws_reducer_ldg(const double* sd, const double* s
     constexpr int HC = C / 2, NT = kWsThreads, NW = kWsT / 32;
     const int rt = threadIdx.x - kWsT;  // 0..127
     const int w = rt >> 5, lane = rt & 31;
+    // a warp's columns (w, w+4, ...) as independent chains (HC = 8 at m <= 1024)
     auto reduce = [&](const double* red, double* bc, double denom, double y) {
-        for (int c = w; c < HC; c += 4) {
-            double q[NW];
+        constexpr int PER = (HC + 3) / 4;
+        double v[PER];
 #pragma unroll
-            for (int k = 0; k < NW; ++k) q[k] = red[c * kWsT + lane + 32 * k];
-            const double v = warp_butterfly32(lane_tree<NW>(q));
-            const double g = PDAS_HOIST_WS ? div_by(v, denom, y) : v / denom;
-            if (lane == 0) bc[c] = g;
+        for (int k = 0; k < PER; ++k) {
+            const int c = w + 4 * k;
+            if (c < HC) {
+                double q[NW];
+#pragma unroll
+                for (int i = 0; i < NW; ++i) q[i] = red[c * kWsT + lane + 32 * i];
+                v[k] = lane_tree<NW>(q);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int c = w + 4 * k;
+            if (c < HC) {
+                const double u = warp_butterfly32(v[k]);
+                const double g = PDAS_HOIST_WS ? div_by(u, denom, y) : u / denom;
+                if (lane == 0) bc[c] = g;
+            }
         }
     };
     bool act = sd[0] != 1.0;
@@ -1040,14 +1072,28 @@ __device__ __forceinline__ void ws_reducer(Pipe<S>& pp, const double* __restrict
     auto wait_stage = [&](int j) {
         if (producer) mbar_wait_a(pp.full_a + 8 * (j % S), (j / S) & 1u);
     };
+    // a warp's columns (w, w+4, ...) as independent chains (HC = 8 at m <= 1024)
     auto reduce = [&](const double* red, double* bc, double denom, double y) {
-        for (int c = w; c < HC; c += 4) {
-            double q[NW];
+        constexpr int PER = (HC + 3) / 4;
+        double v[PER];
 #pragma unroll
-            for (int k = 0; k < NW; ++k) q[k] = red[c * kWsT + lane + 32 * k];
-            const double v = warp_butterfly32(lane_tree<NW>(q));
-            const double g = PDAS_HOIST_WS ? div_by(v, denom, y) : v / denom;
-            if (lane == 0) bc[c] = g;
+        for (int k = 0; k < PER; ++k) {
+            const int c = w + 4 * k;
+            if (c < HC) {
+                double q[NW];
+#pragma unroll
+                for (int i = 0; i < NW; ++i) q[i] = red[c * kWsT + lane + 32 * i];
+                v[k] = lane_tree<NW>(q);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int c = w + 4 * k;
+            if (c < HC) {
+                const double u = warp_butterfly32(v[k]);
+                const double g = PDAS_HOIST_WS ? div_by(u, denom, y) : u / denom;
+                if (lane == 0) bc[c] = g;
+            }
         }
     };
     // prologue: stages 0 .. S-1 in flight; release the compute warps once
@@ -1406,6 +1452,68 @@ static SideStream& side_stream() {
     return s;
 }
 
+// Diagnostics (env PDAS_CASCADE_PROFILE=1): timing events around every
+// update / panel launch of the 1-GPU cascade; the last cascade's rows
+// (kind 0 update / 1 panel, block, start ms, end ms) are read back with
+// pdas_debug_cascade_profile (tools/cascade_timeline.py).  Off: no events.
+struct ProfRow {
+    int kind;
+    idx_t block;
+    cudaEvent_t e[2];
+};
+static std::vector<double> g_prof_rows;
+
+struct CascProfile {
+    bool on;
+    cudaEvent_t t0 = nullptr;
+    std::vector<ProfRow> rows;
+    CascProfile(idx_t nrows, cudaStream_t st) {
+        static const bool env = env_int("PDAS_CASCADE_PROFILE", 0) != 0;
+        on = env;
+        if (!on) return;
+        rows.reserve((size_t)nrows);
+        cudaEventCreate(&t0);
+        cudaEventRecord(t0, st);
+    }
+    void mark(cudaStream_t s, int kind, idx_t b, int which) {
+        if (!on) return;
+        if (which == 0) {
+            ProfRow r{kind, b, {nullptr, nullptr}};
+            cudaEventCreate(&r.e[0]);
+            cudaEventCreate(&r.e[1]);
+            rows.push_back(r);
+            cudaEventRecord(rows.back().e[0], s);
+        } else {
+            for (size_t i = rows.size(); i-- > 0;)
+                if (rows[i].kind == kind && rows[i].block == b) {
+                    cudaEventRecord(rows[i].e[1], s);
+                    break;
+                }
+        }
+    }
+    void finish(cudaStream_t st) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        g_prof_rows.clear();
+        for (auto& r : rows) {
+            float a = 0.f, b = 0.f;
+            cudaEventElapsedTime(&a, t0, r.e[0]);
+            cudaEventElapsedTime(&b, t0, r.e[1]);
+            g_prof_rows.insert(g_prof_rows.end(), {(double)r.kind, (double)r.block, a, b});
+            cudaEventDestroy(r.e[0]);
+            cudaEventDestroy(r.e[1]);
+        }
+        cudaEventDestroy(t0);
+    }
+};
+
+idx_t cascade_profile_rows(double* out, idx_t max_rows) {
+    const idx_t nr = (idx_t)(g_prof_rows.size() / 4);
+    const idx_t k = nr < max_rows ? nr : max_rows;
+    for (idx_t i = 0; i < 4 * k; ++i) out[i] = g_prof_rows[(size_t)i];
+    return nr;
+}
+
 // What to launch: the full cascade, or one building block of the sharded
 // cascade (dist.py): a panel over block [p0,p1) after previous block [q0,p0),
 // or an update of a tile list with block [p0,p1).
@@ -1423,9 +1531,9 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
     constexpr bool GEN = (T == 32);
     static_assert(Cu * G == CT, "tile width");
     const size_t smem_u = casc_smem_bytes<T, Cu, G>(TMA ? S : 0, m);
-    const size_t smem_p = casc_smem_bytes<T, CT, 1>(TMA ? S : 0, m);
+    const size_t smem_p = casc_smem_bytes<T, CT, 1>(TMA && PDAS_PANEL_TMA ? S : 0, m);
     auto ku = k_casc_update<TMA, S, T, R, Cu, G, GEN>;
-    auto kp = k_casc_panel<TMA, S, T, R, CT, GEN>;
+    auto kp = k_casc_panel<TMA && PDAS_PANEL_TMA, S, T, R, CT, GEN>;
     cudaFuncSetAttribute(ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_u);
     cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
     // warp-specialized update for the 256-thread single-group layouts
@@ -1478,10 +1586,13 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         // soon as its 16-odd tiles are done instead of after all of U(b).
         int* uflag = flags + (n + 2);
         cudaMemsetAsync(uflag, 0, sizeof(int) * (size_t)(n + 2), st);
+        CascProfile prof(2 * nb + 1, st);
         cudaEventRecord(ss.e0, st);
         cudaStreamWaitEvent(ss.ps, ss.e0, 0);
+        prof.mark(ss.ps, 1, 0, 0);
         kp<<<(unsigned)tiles_of(0), T, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, 0, 0,
                                                         blk_end(0), fail, flags, epoch, nullptr, 0);
+        prof.mark(ss.ps, 1, 0, 1);
         cudaEventRecord(ss.eP, ss.ps);
         for (idx_t b = 0; b < nb; ++b) {
             cudaStreamWaitEvent(st, ss.eP, 0);  // panel(b): block b is final
@@ -1489,19 +1600,24 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
             // spinning on 16-odd SMs) while U(b-1) still runs
             cudaEventRecord(ss.eU, st);
             const idx_t t0 = b + 1 < nb ? (b + 1) * B / CT : (n + CT - 1) / CT;
+            prof.mark(st, 0, b, 0);
             update(b, t0, uflag);
+            prof.mark(st, 0, b, 1);
             if (b + 1 < nb) {
                 const idx_t p0 = (b + 1) * B;
                 cudaStreamWaitEvent(ss.ps, ss.eU, 0);
+                prof.mark(ss.ps, 1, b + 1, 0);
                 kp<<<(unsigned)tiles_of(b + 1), T, smem_p, ss.ps>>>(
                     cols, a, d, denoms, m, n, p0, p0, blk_end(b + 1), fail, flags, epoch, uflag,
                     (int)(b + 1));
+                prof.mark(ss.ps, 1, b + 1, 1);
                 cudaEventRecord(ss.eP, ss.ps);
             }
         }
         // join: the caller's stream sees every panel
         cudaEventRecord(ss.eP, ss.ps);
         cudaStreamWaitEvent(st, ss.eP, 0);
+        prof.finish(st);
         return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
     }
     cudaEventRecord(ss.e0, st);

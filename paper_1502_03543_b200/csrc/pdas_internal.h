@@ -80,6 +80,7 @@ int launch_cascade_update(double* cols, const double* a, const double* d, idx_t 
 idx_t cascade_supported_m();
 idx_t cascade_flags_count(idx_t m, idx_t n);
 int cascade_tile_width(idx_t m);
+idx_t cascade_profile_rows(double* out, idx_t max_rows);
 constexpr int kCascadeBlock = 128;  // pivots per block (= kMaxBlock in cascade.cu)
 
 // solve_kernels.cu (single right-hand side, latency-optimised)
