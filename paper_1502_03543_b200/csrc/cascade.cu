@@ -595,9 +595,6 @@ __device__ __forceinline__ void apply_global(Tile<T, R, C, GEN>& tl, Pipe<S>& pp
 #ifndef PDAS_WS_LDG
 #define PDAS_WS_LDG 1
 #endif
-#ifndef PDAS_WS_EARLY
-#define PDAS_WS_EARLY 0
-#endif
 constexpr int kWsT = 256;       // compute threads
 constexpr int kWsThreads = 384; // + reducer warpgroup
 #ifndef PDAS_WS_REGS_R
@@ -722,193 +719,19 @@ __device__ __forceinline__ void ws_compute(Tile<kWsT, R, C, false>& tl, const do
     if (a_prev) axpy(HC, bcB);
 }
 
-// Same schedule with the stage reads hoisted one phase earlier: right after
-// GB(j-1), C1(j) issues the shared-memory loads of P_j and A_{j+1} into
-// registers, so C2(j) starts on arithmetic (the reducer makes stage j+1
-// ready before GB(j-1) instead of before GA(j)).
-template <int S, int R, int C, bool FULL>
-__device__ __forceinline__ void ws_compute_early(Tile<kWsT, R, C, false>& tl, const double* buf,
-                                                 int mp, const double* sd, int cnt, double* redA,
-                                                 double* redB, const double* bcA,
-                                                 const double* bcB) {
-    constexpr int HC = C / 2, NT = kWsThreads;
-    const int stage = 2 * mp;
-    double vl[R], vh[R], pl[R], ph[R];
-    double nl[R], nh[R], al[R], ah[R];  // P_j and raw A_{j+1}, loaded ahead
-    auto sptr = [&](int j) -> const double* { return buf + (j % S) * stage; };
-    auto partials = [&](int h0, double* red) {
-#pragma unroll
-        for (int c = 0; c < HC; ++c) {
-            double s[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                double lo = vl[r] * tl.xl[r][h0 + c];
-                double hi = vh[r] * tl.xh[r][h0 + c];
-                s[r] = lo + hi;
-            }
-            red[c * kWsT + tl.t] = lane_tree<R>(s);
-        }
-    };
-    auto axpy = [&](int h0, const double* bc) {
-        double g[HC];
-#pragma unroll
-        for (int c = 0; c < HC; ++c) g[c] = bc[c];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const bool hi = FULL || tl.vhi(r);
-#pragma unroll
-            for (int c = 0; c < HC; ++c) {
-                double q0 = g[c] * pl[r];
-                tl.xl[r][h0 + c] = tl.xl[r][h0 + c] - q0;
-            }
-            if (hi) {
-#pragma unroll
-                for (int c = 0; c < HC; ++c) {
-                    double q1 = g[c] * ph[r];
-                    tl.xh[r][h0 + c] = tl.xh[r][h0 + c] - q1;
-                }
-            }
-        }
-    };
-    // GA(-1): stages 0 and 1 are ready
-    named_bar(3, NT);
-    bool a_prev = false, a_cur = sd[0] != 1.0;
-    if (a_cur) {
-        tl.template make_v<false, FULL>(sptr(0) + mp, sd[0] - 1.0, vl, vh);
-        partials(0, redA);
-    }
-    named_arrive(1, NT);
-    for (int j = 0; j < cnt; ++j) {
-        const double dn = sd[j + 1 < cnt ? j + 1 : j];
-        const bool a_next = j + 1 < cnt && dn != 1.0;
-        // ---- C1(j)
-        WS_MARK(0, j, 0);
-        if (j > 0) named_bar(4, NT);  // gB(j-1) ready, stages j and j+1 ready
-        WS_MARK(0, j, 1);
-        if (a_cur) tl.template load_p<false, FULL>(sptr(j), nl, nh);
-        if (a_next) tl.template load_p<false, FULL>(sptr(j + 1) + mp, al, ah);
-        if (j > 0 && a_prev) axpy(HC, bcB);
-        if (a_cur) partials(HC, redB);
-        named_arrive(2, NT);
-        WS_MARK(0, j, 2);
-        // ---- C2(j)
-        named_bar(3, NT);  // gA(j) ready
-        WS_MARK(0, j, 3);
-        if (a_cur) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                pl[r] = nl[r];
-                ph[r] = nh[r];
-            }
-            axpy(0, bcA);
-        }
-        if (a_next) {
-            const double f = dn - 1.0;
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                vl[r] = al[r] * f;
-                vh[r] = (FULL || tl.vhi(r)) ? ah[r] * f : 0.0;
-            }
-            partials(0, redA);
-        }
-        named_arrive(1, NT);
-        WS_MARK(0, j, 4);
-        a_prev = a_cur;
-        a_cur = a_next;
-    }
-    named_bar(4, NT);
-    if (a_prev) axpy(HC, bcB);
-}
-
-template <int S, int R, int C>
-__device__ __forceinline__ void ws_reducer_early(Pipe<S>& pp, const double* __restrict__ cols,
-                                                 const double* __restrict__ a, idx_t p0, int cnt,
-                                                 int m, const double* redA, const double* redB,
-                                                 double* bcA, double* bcB) {
-    constexpr int HC = C / 2, NT = kWsThreads, NW = kWsT / 32;
-    static_assert(S >= 3, "stages j, j+1, j+2 live at once");
-    const int rt = threadIdx.x - kWsT;  // 0..127
-    const int w = rt >> 5, lane = rt & 31;
-    const bool producer = rt == 0;
-    const double* sd = pp.sd;
-    const double* sden = pp.sden;
-    const double* sy = pp.sy;
-    auto wait_stage = [&](int j) {
-        if (producer) mbar_wait_a(pp.full_a + 8 * (j % S), (j / S) & 1u);
-    };
-    // a warp's columns (w, w+4, ...) as independent chains (HC = 8 at m <= 1024)
-    auto reduce = [&](const double* red, double* bc, double denom, double y) {
-        constexpr int PER = (HC + 3) / 4;
-        double v[PER];
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            const int c = w + 4 * k;
-            if (c < HC) {
-                double q[NW];
-#pragma unroll
-                for (int i = 0; i < NW; ++i) q[i] = red[c * kWsT + lane + 32 * i];
-                v[k] = lane_tree<NW>(q);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            const int c = w + 4 * k;
-            if (c < HC) {
-                const double u = warp_butterfly32(v[k]);
-                const double g = PDAS_HOIST_WS ? div_by(u, denom, y) : u / denom;
-                if (lane == 0) bc[c] = g;
-            }
-        }
-    };
-    if (producer)
-        for (int i = 0; i < (cnt < S ? cnt : S); ++i)
-            pipe_issue(pp, i, cols + (p0 + i) * m, a + (p0 + i) * m, m, false);
-    wait_stage(0);
-    if (cnt > 1) wait_stage(1);
-    named_arrive(3, NT);
-    bool act = sd[0] != 1.0;
-    double den = sden[0], y = sy[0];
-    for (int j = 0; j < cnt; ++j) {
-        const int jn = j + 1 < cnt ? j + 1 : j;
-        const bool act_n = sd[jn] != 1.0;
-        const double den_n = sden[jn], y_n = sy[jn];
-        // ---- R1(j)
-        WS_MARK(1, j, 0);
-        named_bar(1, NT);  // partials A(j) published
-        WS_MARK(1, j, 1);
-        if (act) reduce(redA, bcA, den, y);
-        WS_MARK(1, j, 2);
-        named_arrive(3, NT);
-        WS_MARK(1, j, 3);
-        // ---- R2(j)
-        named_bar(2, NT);  // partials B(j) published; stage j fully read
-        WS_MARK(1, j, 4);
-        if (act) reduce(redB, bcB, den, y);
-        if (j + 2 < cnt) wait_stage(j + 2);  // C1(j+1) reads A_{j+2}
-        named_arrive(4, NT);
-        WS_MARK(1, j, 5);
-        if (producer && j + S < cnt)
-            pipe_issue(pp, j + S, cols + (p0 + j + S) * m, a + (p0 + j + S) * m, m, false);
-        act = act_n;
-        den = den_n;
-        y = y_n;
-    }
-    named_bar(1, NT);  // the compute warps' final PA arrival
-}
-
 // Direct-load variant: P_l and A[:,l] go L2 -> registers (ld.global.cg), one
 // pivot ahead, instead of through a TMA ring in shared memory.  Shared-memory
 // traffic per pivot drops from ~100 KB (TMA writes + stage reads +
 // reductions) to the 32 KB of the reductions; the reducer warpgroup only
 // reduces.  Same arithmetic, same order.
-template <int R, int C, bool FULL>
-__device__ __forceinline__ void ws_compute_ldg(Tile<kWsT, R, C, false>& tl,
+template <int R, int C, bool FULL, int TC = kWsT>
+__device__ __forceinline__ void ws_compute_ldg(Tile<TC, R, C, false>& tl,
                                                const double* __restrict__ pcol,
                                                const double* __restrict__ acol, int m,
                                                const double* sd, int cnt, double* redA,
                                                double* redB, const double* bcA,
                                                const double* bcB) {
-    constexpr int HC = C / 2, NT = kWsThreads;
+    constexpr int HC = C / 2, NT = TC + 128;
     double vl[R], vh[R], pl[R], ph[R];
     double npl[R], nph[R], nal[R], nah[R];  // P_{j+1}, raw A_{j+2} in flight
     auto partials = [&](int h0, double* red) {
@@ -921,7 +744,7 @@ __device__ __forceinline__ void ws_compute_ldg(Tile<kWsT, R, C, false>& tl,
                 double hi = vh[r] * tl.xh[r][h0 + c];
                 s[r] = lo + hi;
             }
-            red[c * kWsT + tl.t] = lane_tree<R>(s);
+            red[c * TC + tl.t] = lane_tree<R>(s);
         }
     };
     auto axpy = [&](int h0, const double* bc) {
@@ -1001,12 +824,12 @@ __device__ __forceinline__ void ws_compute_ldg(Tile<kWsT, R, C, false>& tl,
     if (a_prev) axpy(HC, bcB);
 }
 
-template <int R, int C>
+template <int R, int C, int TC = kWsT>
 __device__ __forceinline__ void ws_reducer_ldg(const double* sd, const double* sden,
                                                const double* sy, int cnt, const double* redA,
                                                const double* redB, double* bcA, double* bcB) {
-    constexpr int HC = C / 2, NT = kWsThreads, NW = kWsT / 32;
-    const int rt = threadIdx.x - kWsT;  // 0..127
+    constexpr int HC = C / 2, NT = TC + 128, NW = TC / 32;
+    const int rt = threadIdx.x - TC;  // 0..127
     const int w = rt >> 5, lane = rt & 31;
     // a warp's columns (w, w+4, ...) as independent chains (HC = 8 at m <= 1024)
     auto reduce = [&](const double* red, double* bc, double denom, double y) {
@@ -1018,7 +841,7 @@ __device__ __forceinline__ void ws_reducer_ldg(const double* sd, const double* s
             if (c < HC) {
                 double q[NW];
 #pragma unroll
-                for (int i = 0; i < NW; ++i) q[i] = red[c * kWsT + lane + 32 * i];
+                for (int i = 0; i < NW; ++i) q[i] = red[c * TC + lane + 32 * i];
                 v[k] = lane_tree<NW>(q);
             }
         }
@@ -1173,8 +996,6 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kWsRegsReducer));
         if constexpr (PDAS_WS_LDG && R <= 4)
             ws_reducer_ldg<R, C>(pp.sd, pp.sden, pp.sy, cnt, redA, redB, bcA, bcB);
-        else if constexpr (PDAS_WS_EARLY && S >= 3 && R <= 4)
-            ws_reducer_early<S, R, C>(pp, cols, a, p0, cnt, m, redA, redB, bcA, bcB);
         else
             ws_reducer<S, R, C>(pp, cols, a, p0, cnt, m, redA, redB, bcA, bcB);
         return;
@@ -1192,11 +1013,6 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             ws_compute_ldg<R, C, true>(tl, pc, ac, m, pp.sd, cnt, redA, redB, bcA, bcB);
         else
             ws_compute_ldg<R, C, false>(tl, pc, ac, m, pp.sd, cnt, redA, redB, bcA, bcB);
-    } else if constexpr (PDAS_WS_EARLY && S >= 3 && R <= 4) {
-        if (full)
-            ws_compute_early<S, R, C, true>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
-        else
-            ws_compute_early<S, R, C, false>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
     } else {
         if (full)
             ws_compute<S, R, C, true>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
