@@ -118,6 +118,16 @@ int64_t pdas_cascade_ws_bytes(int64_t m, int64_t n);
 int pdas_solve_sweeps_ws(double* cols, const double* a, const double* d, int64_t m, int64_t n,
                          void* ws, int32_t epoch, int32_t* fail_dev, void* stream);
 
+/* init_workspace's x0 solve fused with the cascade (normal.py:115-124 then
+ * :163-175): on entry column n of cols holds the right-hand side A x; the
+ * library solves x0 = L0^-T L0^-1 rhs into it (same rounding sequence as
+ * cholesky_solve_many with k = 1) and runs the cascade.  When column n sits
+ * alone in the last column tile the x0 solve and that tile's updates run on
+ * their own stream, overlapped with the Y part of the cascade. */
+int pdas_solve_sweeps_ws_x0(double* cols, const double* a, const double* d, const double* low,
+                            int64_t m, int64_t n, void* ws, int32_t epoch, int32_t* fail_dev,
+                            void* stream);
+
 /* Building blocks of the cascade for column-sharded (multi-GPU) execution,
  * parallel.py:1-7 / the per-step column independence of _kernels.pyx:260-289.
  * Pivots come in blocks of pdas_cascade_block_pivots(); columns in tiles of

@@ -72,6 +72,8 @@ SIGNATURES = {
     "pdas_solve_sweeps": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _I64, _I64, ctypes.c_int, _VP, _VP]),
     "pdas_cascade_ws_bytes": (ctypes.c_int64, [_I64, _I64]),
     "pdas_solve_sweeps_ws": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, _VP, ctypes.c_int32, _VP, _VP]),
+    "pdas_solve_sweeps_ws_x0": (ctypes.c_int, [_VP, _VP, _VP, _VP, _I64, _I64, _VP, ctypes.c_int32,
+                                               _VP, _VP]),
     "pdas_cascade_tile_width": (ctypes.c_int, [_I64]),
     "pdas_cascade_block_pivots": (ctypes.c_int, []),
     "pdas_cascade_panel": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, _I64, _I64, _I64, _VP,

@@ -194,6 +194,25 @@ int pdas_solve_sweeps_ws(double* cols, const double* a, const double* d, int64_t
         "solve_sweeps");
 }
 
+int pdas_solve_sweeps_ws_x0(double* cols, const double* a, const double* d, const double* low,
+                            int64_t m, int64_t n, void* ws, int32_t epoch, int32_t* fail_dev,
+                            void* stream) {
+    if (m < 1 || n < 0 || fail_dev == nullptr || ws == nullptr || epoch < 1 || low == nullptr)
+        return set_err(PDAS_ERR_ARG, "solve_sweeps_ws_x0: bad args");
+    if (m > pdas::cascade_supported_m())
+        return set_err(PDAS_ERR_UNSUPPORTED, "solve_sweeps: m above the compiled configurations");
+    const int64_t nd = n > 0 ? n : 1;
+    double* denoms = static_cast<double*>(ws);
+    int* flags = reinterpret_cast<int*>(static_cast<unsigned char*>(ws) + ((nd * 8 + 255) / 256) * 256);
+    double* work = nullptr;
+    int rc = scratch(&work, (size_t)pdas::solve_one_work_doubles(m), S(stream));
+    if (rc) return rc;
+    rc = pdas::launch_cascade_x0(cols, a, d, low, m, n, denoms, fail_dev, flags, epoch, work,
+                                 S(stream));
+    if (work) cudaFreeAsync(work, S(stream));
+    return check_cuda(rc, "solve_sweeps_ws_x0");
+}
+
 int pdas_cascade_tile_width(int64_t m) {
     if (m < 1 || m > pdas::cascade_supported_m()) return 0;
     return pdas::cascade_tile_width(m);

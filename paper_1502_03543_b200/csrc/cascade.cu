@@ -1248,8 +1248,9 @@ idx_t cascade_supported_m() { return 16384; }
 
 // Side stream (high priority) + events for the panel lookahead, per device.
 struct SideStream {
-    cudaStream_t ps = nullptr;
-    cudaEvent_t e0 = nullptr, eP = nullptr, eU = nullptr;
+    cudaStream_t ps = nullptr;  // panels (high priority)
+    cudaStream_t xs = nullptr;  // x0 solve + the x tile's updates (see CascOp::x0_low)
+    cudaEvent_t e0 = nullptr, eP = nullptr, eU = nullptr, eX = nullptr;
 };
 
 static SideStream& side_stream() {
@@ -1261,6 +1262,8 @@ static SideStream& side_stream() {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
         cudaStreamCreateWithPriority(&s.ps, cudaStreamNonBlocking, hi);
+        cudaStreamCreateWithPriority(&s.xs, cudaStreamNonBlocking, hi);
+        cudaEventCreateWithFlags(&s.eX, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&s.e0, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&s.eP, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&s.eU, cudaEventDisableTiming);
@@ -1338,6 +1341,11 @@ struct CascOp {
     idx_t q0 = 0, p0 = 0, p1 = 0;
     const int64_t* tiles = nullptr;
     idx_t ntiles = 0;
+    // kind 0 only: column n holds the right-hand side; x0 = L^-T L^-1 rhs
+    // (normal.py:123) is solved here, concurrently with the Y part of the
+    // cascade, when column n sits alone in the last tile (n % CT == 0).
+    const double* x0_low = nullptr;
+    double* x0_work = nullptr;
 };
 
 template <bool TMA, int S, int T, int R, int Cu, int G, int CT>
@@ -1403,13 +1411,37 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         int* uflag = flags + (n + 2);
         cudaMemsetAsync(uflag, 0, sizeof(int) * (size_t)(n + 2), st);
         CascProfile prof(2 * nb + 1, st);
+        // x lane: column n alone in the last tile -> the x0 solve and that
+        // tile's updates run on their own stream, off the Y critical path
+        const bool xlane = op.x0_low != nullptr && n % CT == 0;
+        const idx_t nt_y = xlane ? ntiles - 1 : ntiles;  // tiles U(b) covers
+        auto update_x = [&](idx_t b) {  // block b -> the x tile (1 CTA)
+            if (use_ws)
+                kws<<<1, kWsThreads, smem_ws, ss.xs>>>(cols, a, d, denoms, m, n, b * B, blk_end(b),
+                                                       ntiles - 1, fail, nullptr, nullptr, 0, 0);
+            else
+                ku<<<1, T * G, smem_u, ss.xs>>>(cols, a, d, denoms, m, n, b * B, blk_end(b),
+                                                ntiles - 1, fail, nullptr, nullptr, 0, 0);
+        };
         cudaEventRecord(ss.e0, st);
         cudaStreamWaitEvent(ss.ps, ss.e0, 0);
+        if (op.x0_low) {
+            cudaStreamWaitEvent(ss.xs, ss.e0, 0);
+            launch_solve_one(op.x0_low, m, cols + (size_t)n * m, op.x0_work, xlane ? ss.xs : st);
+            if (!xlane) {  // sequential fallback: the panels wait for x0 too
+                cudaEventRecord(ss.e0, st);
+                cudaStreamWaitEvent(ss.ps, ss.e0, 0);
+            }
+        }
         prof.mark(ss.ps, 1, 0, 0);
         kp<<<(unsigned)tiles_of(0), T, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, 0, 0,
                                                         blk_end(0), fail, flags, epoch, nullptr, 0);
         prof.mark(ss.ps, 1, 0, 1);
         cudaEventRecord(ss.eP, ss.ps);
+        if (xlane) {
+            cudaStreamWaitEvent(ss.xs, ss.eP, 0);
+            update_x(0);
+        }
         for (idx_t b = 0; b < nb; ++b) {
             cudaStreamWaitEvent(st, ss.eP, 0);  // panel(b): block b is final
             // eU marks the START of U(b): panel(b+1) must not be resident (and
@@ -1417,7 +1449,17 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
             cudaEventRecord(ss.eU, st);
             const idx_t t0 = b + 1 < nb ? (b + 1) * B / CT : (n + CT - 1) / CT;
             prof.mark(st, 0, b, 0);
-            update(b, t0, uflag);
+            if (t0 < nt_y) {
+                const int uc = b + 1 < nb ? (int)tiles_of(b + 1) : 0;
+                if (use_ws)
+                    kws<<<(unsigned)(nt_y - t0), kWsThreads, smem_ws, st>>>(
+                        cols, a, d, denoms, m, n, b * B, blk_end(b), t0, fail, nullptr, uflag,
+                        (int)(b + 1), uc);
+                else
+                    ku<<<(unsigned)(nt_y - t0), T * G, smem_u, st>>>(
+                        cols, a, d, denoms, m, n, b * B, blk_end(b), t0, fail, nullptr, uflag,
+                        (int)(b + 1), uc);
+            }
             prof.mark(st, 0, b, 1);
             if (b + 1 < nb) {
                 const idx_t p0 = (b + 1) * B;
@@ -1428,11 +1470,19 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
                     (int)(b + 1));
                 prof.mark(ss.ps, 1, b + 1, 1);
                 cudaEventRecord(ss.eP, ss.ps);
+                if (xlane) {
+                    cudaStreamWaitEvent(ss.xs, ss.eP, 0);
+                    update_x(b + 1);
+                }
             }
         }
-        // join: the caller's stream sees every panel
+        // join: the caller's stream sees every panel and the x lane
         cudaEventRecord(ss.eP, ss.ps);
         cudaStreamWaitEvent(st, ss.eP, 0);
+        if (op.x0_low) {
+            cudaEventRecord(ss.eX, ss.xs);
+            cudaStreamWaitEvent(st, ss.eX, 0);
+        }
         prof.finish(st);
         return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
     }
@@ -1535,6 +1585,24 @@ int launch_cascade(double* cols, const double* a, const double* d, idx_t m, idx_
     if (n == 0) return PDAS_OK;
     const int B = block_pivots > 0 ? block_pivots : env_int("PDAS_CASCADE_BLOCK", 128);
     return dispatch_cascade(cols, a, d, m, n, denoms, fail_dev, flags, epoch, B, st, CascOp{});
+}
+
+int launch_cascade_x0(double* cols, const double* a, const double* d, const double* low, idx_t m,
+                      idx_t n, double* denoms, int32_t* fail_dev, int* flags, int epoch,
+                      double* work, cudaStream_t st) {
+    if (m < 1 || n < 0 || m > INT_MAX / 4) return PDAS_ERR_ARG;
+    cudaMemsetAsync(fail_dev, 0, sizeof(int32_t), st);
+    if (n == 0) return launch_solve_one(low, m, cols, work, st);
+    CascOp op;
+    op.x0_low = low;
+    op.x0_work = work;
+    const int B = env_int("PDAS_CASCADE_BLOCK", 128);
+    if (!PDAS_CASC_EARLYPANEL) {  // the x lane exists in the early-panel schedule only
+        int rc = launch_solve_one(low, m, cols + (size_t)n * m, work, st);
+        if (rc) return rc;
+        op = CascOp{};
+    }
+    return dispatch_cascade(cols, a, d, m, n, denoms, fail_dev, flags, epoch, B, st, op);
 }
 
 int launch_cascade_panel(double* cols, const double* a, const double* d, idx_t m, idx_t n,

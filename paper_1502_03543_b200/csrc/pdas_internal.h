@@ -71,6 +71,9 @@ int launch_sweep_phase2(double* cols, idx_t m, idx_t l0, const double* inner, do
 int launch_cascade(double* cols, const double* a, const double* d, idx_t m, idx_t n,
                    double* denoms, int32_t* fail_dev, int* flags, int epoch, int block_pivots,
                    cudaStream_t st);
+int launch_cascade_x0(double* cols, const double* a, const double* d, const double* low, idx_t m,
+                      idx_t n, double* denoms, int32_t* fail_dev, int* flags, int epoch,
+                      double* work, cudaStream_t st);
 int launch_cascade_panel(double* cols, const double* a, const double* d, idx_t m, idx_t n,
                          idx_t q0, idx_t p0, idx_t p1, double* denoms, int32_t* fail_dev,
                          int* flags, int epoch, cudaStream_t st);

@@ -331,6 +331,13 @@ class ShardedSolver(DeviceSolver):
         run_collective(self.plan, self.shard, self.group)
         self.launches += self._casc_launches
 
+    def _cascade_x0(self) -> None:
+        from .engine import d_solve_many
+
+        d_solve_many(self.basis.L0, self.m, self.xcol, 1)  # replicated x0 (normal.py:123)
+        self.launches += 2
+        self._cascade()
+
 
 def solve_sweeps_virtual(cols: np.ndarray, a: np.ndarray, d: np.ndarray, world: int,
                          block: Optional[int] = None) -> Tuple[int, List[np.ndarray]]:

@@ -244,6 +244,16 @@ class DeviceSolver:
              n, dv.ptr(self.casc_ws), self.epoch, self._sptr(OFF_CASCADE_FAIL), dv.stream())
         self.launches += 2 * ((n + 127) // 128)
 
+    def _cascade_x0(self) -> None:
+        """x0 = L0^-T L0^-1 rhs (normal.py:123) fused with the cascade: the
+        library overlaps the x0 solve with the Y part when it can."""
+        m, n = self.m, self.n
+        self.epoch += 1
+        call("pdas_solve_sweeps_ws_x0", dv.ptr(self.cols), dv.ptr(self.prob.A), dv.ptr(self.d),
+             dv.ptr(self.basis.L0), m, n, dv.ptr(self.casc_ws), self.epoch,
+             self._sptr(OFF_CASCADE_FAIL), dv.stream())
+        self.launches += 2 + 3 * ((n + 127) // 128)
+
     def enqueue_solve(self) -> None:
         """Scaling, rhs and the normal-equations solve (cascade or direct)."""
         st = dv.stream()
@@ -257,9 +267,7 @@ class DeviceSolver:
             B = self.basis
             self.cols[:m * n].copy_(B.Y, non_blocking=True)  # init_workspace (normal.py:121-123)
             self.xcol.copy_(self.rhs, non_blocking=True)
-            d_solve_many(B.L0, m, self.xcol, 1)  # k_fwd_one + k_bwd_one
-            self.launches += 2
-            self._cascade()
+            self._cascade_x0()
             self.dy = self.xcol
         else:
             self._solve_direct_into(self.dy_direct, self._sptr(OFF_CHOL_FAIL))
