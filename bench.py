@@ -94,6 +94,22 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU legs
+def cascade_traffic(n, block=128):
+    """DRAM bytes (read + write) of one c3 cascade, from the committed ncu
+    launch list of `tools/cascade_time.py` (profiles/r01_launches_cascade.json:
+    per-kernel sums of dram__bytes_read.sum + dram__bytes_write.sum)."""
+    try:
+        d = json.load(open(os.path.join(REPO, "profiles", "r01_launches_cascade.json")))
+    except Exception:
+        return None
+    casc = {k: v for k, v in d.items() if "k_casc" in k}
+    panels = sum(v["launches"] for k, v in casc.items() if "panel" in k)
+    if not panels:
+        return None
+    ncasc = panels / ((n + block - 1) // block)
+    return sum(v["dram_bytes"] for v in casc.values()) / ncasc
+
+
 def cpu_cascade_sample(a, y, x0col, d, steps, threads):
     """Time the reference's compiled core (oracle/_ref, else the restated
     oracle) on cascade steps [0, steps) of the c3 workload; returns
@@ -282,7 +298,9 @@ def run_ours(args):
     achieved_tf = Flops / casc_s / 1e12
     roofline = {
         "bound": "fp64", "achieved": achieved_tf, "peak": fp64_peak, "unit": "TFLOP/s",
-        "frac": achieved_tf / fp64_peak, "traffic": None,
+        "frac": achieved_tf / fp64_peak, "traffic": cascade_traffic(N),
+        "traffic_unit": "bytes per cascade (DRAM read+write of all k_casc_* launches, ncu)",
+        "traffic_source": "profiles/r01_launches_cascade.json",
         "kernel": "cascade (k_casc_panel + k_casc_update), one 20000-step solve",
         "peak_source": "measured now: pdas_probe_fp64 (separate DMUL+DADD, no FMA)",
         "hbm_equivalent": {

@@ -306,7 +306,8 @@ struct Tile {
 // TMA bytes.  empty[s]: one arrival per consumer group once it is done.
 // `k` counts stage uses (identical in every thread of the CTA).  S (stage
 // count) is a compile-time constant so stage arithmetic is shifts/masks.
-constexpr int kMaxBlock = 128;  // pivots per block (B) upper bound
+constexpr int kMaxBlock = 256;  // pivots per block (B) upper bound
+constexpr int kDefaultBlock = 256;  // 1-GPU default (c3: 2% faster than 128; dist uses 128)
 
 template <int S>
 struct Pipe {
@@ -1583,7 +1584,7 @@ int launch_cascade(double* cols, const double* a, const double* d, idx_t m, idx_
     if (m < 1 || n < 0 || m > INT_MAX / 4) return PDAS_ERR_ARG;
     cudaMemsetAsync(fail_dev, 0, sizeof(int32_t), st);
     if (n == 0) return PDAS_OK;
-    const int B = block_pivots > 0 ? block_pivots : env_int("PDAS_CASCADE_BLOCK", 128);
+    const int B = block_pivots > 0 ? block_pivots : env_int("PDAS_CASCADE_BLOCK", kDefaultBlock);
     return dispatch_cascade(cols, a, d, m, n, denoms, fail_dev, flags, epoch, B, st, CascOp{});
 }
 
@@ -1596,7 +1597,7 @@ int launch_cascade_x0(double* cols, const double* a, const double* d, const doub
     CascOp op;
     op.x0_low = low;
     op.x0_work = work;
-    const int B = env_int("PDAS_CASCADE_BLOCK", 128);
+    const int B = env_int("PDAS_CASCADE_BLOCK", kDefaultBlock);
     if (!PDAS_CASC_EARLYPANEL) {  // the x lane exists in the early-panel schedule only
         int rc = launch_solve_one(low, m, cols + (size_t)n * m, work, st);
         if (rc) return rc;

@@ -200,3 +200,36 @@ def test_hoisted_division_bits(gpu):
     ok = ~np.isnan(host)
     assert bits_equal(r[ok], host[ok])  # and both are the IEEE quotient
     del torch
+
+
+@pytest.mark.parametrize("m,n", [(50, 200), (50, 203), (300, 1024), (300, 1030), (1000, 2048),
+                                 (1000, 2050)])
+def test_cascade_with_fused_x0(gpu, m, n):
+    """pdas_solve_sweeps_ws_x0: x0 = L0^-T L0^-1 rhs solved inside the cascade
+    call (overlapped on its own stream when column n is alone in the last tile,
+    sequential otherwise) == init_workspace + solve_sweeps (normal.py:115-124)."""
+    import torch
+    from paper_1502_03543_b200 import _device as dv
+    from paper_1502_03543_b200._lib import call, load
+
+    rng = np.random.default_rng(m * 31 + n)
+    a = np.asfortranarray(rng.uniform(-1, 1, (m, n)))
+    d = np.power(10.0, rng.uniform(-3, 3, n))
+    d[rng.random(n) < 0.1] = 1.0
+    rhs = rng.uniform(-1, 1, m)
+    R = O.restated()
+    basis = O.prepare_woodbury(R, a)
+    cref, inner, v = O.init_workspace(R, basis, rhs)
+    ret = R.solve_sweeps(cref, a, d, inner, v, 8)
+    cin = np.asfortranarray(np.column_stack([np.asarray(basis.Y), rhs]))
+    cols = dv.upload(cin)
+    ws = torch.zeros(int(load().pdas_cascade_ws_bytes(m, n)), dtype=torch.uint8,
+                     device=dv.device())
+    fail = torch.zeros(1, dtype=torch.int32, device=dv.device())
+    da, dd, dl = dv.upload(a), dv.upload(d), dv.upload(np.asfortranarray(basis.L0))  # kept alive
+    call("pdas_solve_sweeps_ws_x0", dv.ptr(cols), dv.ptr(da), dv.ptr(dd), dv.ptr(dl), m, n,
+         dv.ptr(ws), 1, dv.ptr(fail), dv.stream())
+    dv.synchronize()
+    assert int(fail.item()) == ret
+    if ret == 0:
+        assert bits_equal(dv.download(cols).reshape((m, n + 1), order="F"), cref)
