@@ -94,7 +94,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU legs
-def cascade_traffic(n, block=128):
+def cascade_traffic(n, block=256):
     """DRAM bytes (read + write) of one c3 cascade, from the committed ncu
     launch list of `tools/cascade_time.py` (profiles/r01_launches_cascade.json:
     per-kernel sums of dram__bytes_read.sum + dram__bytes_write.sum)."""
