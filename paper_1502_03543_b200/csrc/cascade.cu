@@ -55,6 +55,13 @@
 
 namespace pdas {
 
+#ifndef PDAS_PANEL_TRACE
+#define PDAS_PANEL_TRACE 0
+#endif
+#if PDAS_PANEL_TRACE
+__device__ long long g_panel_trace[8];
+#endif
+
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -430,6 +437,22 @@ __device__ __forceinline__ void apply_impl(Tile<T, R, C, GEN>& tl, Pipe<S>& pp,
     const double* ga = a + l0 * m;      // global A column of pivot l0 + j: ga + j*m
     const double* gc = cols + l0 * m;   // global P column
     const int stage = 2 * pp.mp;
+#if PDAS_PANEL_TRACE
+    const bool trace = gridDim.x == 32 && blockIdx.x == 31 && threadIdx.x == 0 && T == 256;
+    long long tm = clock64();
+#define APPLY_LAP(k)                                    \
+    do {                                                \
+        if (trace) {                                    \
+            const long long tn = clock64();             \
+            g_panel_trace[k] += tn - tm;                \
+            tm = tn;                                    \
+        }                                               \
+    } while (0)
+#else
+#define APPLY_LAP(k) \
+    do {             \
+    } while (0)
+#endif
     for (int j = 0; j < cnt; ++j) {
         const unsigned use = k0 + j;
         const double* pc;
@@ -443,6 +466,7 @@ __device__ __forceinline__ void apply_impl(Tile<T, R, C, GEN>& tl, Pipe<S>& pp,
             pc = gc + (size_t)j * m;
             ac = ga + (size_t)j * m;
         }
+        APPLY_LAP(4);  // stage wait
         const double dl = sd[j];
         const bool active = dl != 1.0;
         double part[C];
@@ -453,6 +477,7 @@ __device__ __forceinline__ void apply_impl(Tile<T, R, C, GEN>& tl, Pipe<S>& pp,
             tl.publish(part);
         }
         tl.sync();  // B1: partials published; stage of use-1 fully consumed
+        APPLY_LAP(5);  // partials + B1
         if (TMA && j > 0) {
             if (tl.t == 0) mbar_arrive_a(pp.empty_a + 8 * ((use - 1) % S));
             if (producer && j - 1 + S < cnt)
@@ -462,9 +487,11 @@ __device__ __forceinline__ void apply_impl(Tile<T, R, C, GEN>& tl, Pipe<S>& pp,
         if (active) {
             double g[C];
             tl.template finish<true>(part, sden[j], sy[j], g);
+            APPLY_LAP(6);  // refill + reduction + B2
             double pl[R], ph[R];
             tl.template load_p<!TMA, FULL>(pc, pl, ph);
             tl.template axpy<FULL>(g, pl, ph);
+            APPLY_LAP(7);  // axpy
         }
     }
     if (TMA) {
@@ -1070,6 +1097,102 @@ __global__ void __launch_bounds__(T* G, 1)
     }
 }
 
+// ------------------------------------------------------------ panel triangle
+// The panel's in-register triangle over its own pivot columns [col0, min(col0+C, p1)):
+// for each pivot in order, the live columns' inner products, the breakdown
+// test (first failing step -> *fail = l + 1), the denominator, and the
+// rank-one update of the later columns.  pp.sd is indexed l - q0.  Returns
+// true on breakdown (the tile must then not be stored).
+template <bool TMA, int S, int T, int R, int C, bool GEN>
+__device__ __forceinline__ bool panel_triangle(Tile<T, R, C, GEN>& tl, Pipe<S>& pp,
+                                               const double* __restrict__ a,
+                                               double* __restrict__ denoms, int m, idx_t col0,
+                                               idx_t p1, idx_t q0, int32_t* __restrict__ fail,
+                                               double* bc, bool producer) {
+    // triangle over this tile's own pivot columns, A columns via the pipe
+    const int cnt = (int)((col0 + C < p1 ? col0 + C : p1) - col0);
+    const unsigned k0 = pp.k;
+    if (TMA && producer) {
+        const int pre = cnt < S ? cnt : S;
+        for (int i = 0; i < pre; ++i) pipe_issue(pp, k0 + i, nullptr, a + (col0 + i) * m, m);
+    }
+    bool broken = false;
+#pragma unroll
+    for (int cl = 0; cl < C; ++cl) {
+        if (cl < cnt) {
+            const idx_t l = col0 + cl;
+            const unsigned use = k0 + cl;
+            const double* ac = a + l * m;
+            if (TMA) {
+                const int s = (int)(use % S);
+                mbar_wait(pp.full + s, (use / S) & 1u);
+                ac = pp.buf + (size_t)s * 2 * pp.mp + pp.mp;
+            }
+            const double dl = pp.sd[l - q0];
+            const bool active = dl != 1.0 && !broken;
+            double part[C];
+            if (active) {
+                double vl[R], vh[R];
+                tl.template make_v<!TMA, false>(ac, dl - 1.0, vl, vh);
+                tl.partials(vl, vh, part, cl);  // columns < cl are final
+                tl.publish(part, cl);
+            }
+            tl.sync();
+            if (TMA && cl > 0) {
+                if (producer) mbar_arrive(pp.empty + (int)((use - 1) % S));
+                if (producer && cl - 1 + S < cnt)
+                    pipe_issue(pp, use - 1 + S, nullptr, a + (l - 1 + S) * m, m);
+            }
+            if (active) {
+                double inner[C];
+                tl.template finish<false>(part, 0.0, 0.0, inner, cl);
+                const double denom = 1.0 + inner[cl];
+                if (fabs(denom) <= kDenomEpsRel * (1.0 + fabs(inner[cl]))) {
+                    if (producer) *fail = (int32_t)(l + 1);
+                    broken = true;
+                } else {
+                    if (producer) denoms[l] = denom;
+                    const double yd = div_recip(denom);
+                    double pl[R], ph[R];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        pl[r] = tl.xl[r][cl];
+                        ph[r] = tl.xh[r][cl];
+                    }
+                    // T > 32: one thread per live column divides, all read the
+                    // quotients back (instead of every thread dividing them all)
+                    if (T > 32 && cl + 1 < C) {
+                        if (threadIdx.x > cl && threadIdx.x < C) bc[C + threadIdx.x] = bc[threadIdx.x] / denom;
+                        tl.sync();
+                    }
+#pragma unroll
+                    for (int c = cl + 1; c < C; ++c) {
+                        const double g = T > 32 ? bc[C + c]
+                                         : (PDAS_HOIST_TRI ? div_by(inner[c], denom, yd) : inner[c] / denom);
+#pragma unroll
+                        for (int r = 0; r < R; ++r) {
+                            if (tl.vlo(r)) {
+                                double q0v = g * pl[r];
+                                tl.xl[r][c] = tl.xl[r][c] - q0v;
+                            }
+                            if (tl.vhi(r)) {
+                                double q1v = g * ph[r];
+                                tl.xh[r][c] = tl.xh[r][c] - q1v;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+    }
+    if (TMA) {
+        tl.sync();
+        if (producer) mbar_arrive(pp.empty + (int)((k0 + cnt - 1) % S));
+        pp.k = k0 + cnt;
+    }
+    return broken;
+}
+
 // ------------------------------------------------------------ panel kernel
 // One CTA per tile of block [p0, p1): apply the previous block [q0, p0),
 // then the pivots of this block's earlier tiles as their CTAs publish them
@@ -1113,10 +1236,27 @@ __global__ void __launch_bounds__(T, 1)
         tl.load(cols, col0, n + 1);
         apply_global<TMA>(tl, pp, cols, a, q0, q0, p0, producer);
     }
+#if PDAS_PANEL_TRACE
+    // last CTA of a full panel: cycles spent waiting for predecessors (flag
+    // acquire) vs applying their pivots vs the triangle
+    const bool trace = PDAS_PANEL_TRACE && gridDim.x == 32 && blockIdx.x == 31 && threadIdx.x == 0;
+    long long t_wait = 0, t_apply = 0, t_mark = clock64();
+#define PANEL_LAP(acc)                      \
+    do {                                    \
+        const long long t_now = clock64(); \
+        acc += t_now - t_mark;              \
+        t_mark = t_now;                     \
+    } while (0)
+#else
+#define PANEL_LAP(acc) \
+    do {               \
+    } while (0)
+#endif
     for (idx_t tp = p0 / C; tp < tile && !dead; ++tp) {
         if (producer)
             while (ld_acquire(flags + tp) != epoch) __nanosleep(32);
         __syncthreads();
+        PANEL_LAP(t_wait);
         if (*(volatile int32_t*)fail) {
             dead = true;
             break;
@@ -1130,90 +1270,23 @@ __global__ void __launch_bounds__(T, 1)
         fence_proxy_async_global();  // peer CTA's generic stores -> our TMA reads
         __syncthreads();
         apply_global<TMA>(tl, pp, cols, a, q0, tp * C, e, producer);
+        PANEL_LAP(t_apply);
     }
     if (!dead) {
-        // triangle over this tile's own pivot columns, A columns via the pipe
-        const int cnt = (int)((col0 + C < p1 ? col0 + C : p1) - col0);
-        const unsigned k0 = pp.k;
-        if (TMA && producer) {
-            const int pre = cnt < S ? cnt : S;
-            for (int i = 0; i < pre; ++i) pipe_issue(pp, k0 + i, nullptr, a + (col0 + i) * m, m);
-        }
-        bool broken = false;
-#pragma unroll
-        for (int cl = 0; cl < C; ++cl) {
-            if (cl < cnt) {
-                const idx_t l = col0 + cl;
-                const unsigned use = k0 + cl;
-                const double* ac = a + l * m;
-                if (TMA) {
-                    const int s = (int)(use % S);
-                    mbar_wait(pp.full + s, (use / S) & 1u);
-                    ac = pp.buf + (size_t)s * 2 * pp.mp + pp.mp;
-                }
-                const double dl = pp.sd[l - q0];
-                const bool active = dl != 1.0 && !broken;
-                double part[C];
-                if (active) {
-                    double vl[R], vh[R];
-                    tl.template make_v<!TMA, false>(ac, dl - 1.0, vl, vh);
-                    tl.partials(vl, vh, part, cl);  // columns < cl are final
-                    tl.publish(part, cl);
-                }
-                tl.sync();
-                if (TMA && cl > 0) {
-                    if (producer) mbar_arrive(pp.empty + (int)((use - 1) % S));
-                    if (producer && cl - 1 + S < cnt)
-                        pipe_issue(pp, use - 1 + S, nullptr, a + (l - 1 + S) * m, m);
-                }
-                if (active) {
-                    double inner[C];
-                    tl.template finish<false>(part, 0.0, 0.0, inner, cl);
-                    const double denom = 1.0 + inner[cl];
-                    if (fabs(denom) <= kDenomEpsRel * (1.0 + fabs(inner[cl]))) {
-                        if (producer) *fail = (int32_t)(l + 1);
-                        broken = true;
-                    } else {
-                        if (producer) denoms[l] = denom;
-                        const double yd = div_recip(denom);
-                        double pl[R], ph[R];
-#pragma unroll
-                        for (int r = 0; r < R; ++r) {
-                            pl[r] = tl.xl[r][cl];
-                            ph[r] = tl.xh[r][cl];
-                        }
-                        // T > 32: one thread per live column divides, all read the
-                        // quotients back (instead of every thread dividing them all)
-                        if (T > 32 && cl + 1 < C) {
-                            if (threadIdx.x > cl && threadIdx.x < C) bc[C + threadIdx.x] = bc[threadIdx.x] / denom;
-                            tl.sync();
-                        }
-#pragma unroll
-                        for (int c = cl + 1; c < C; ++c) {
-                            const double g = T > 32 ? bc[C + c]
-                                             : (PDAS_HOIST_TRI ? div_by(inner[c], denom, yd) : inner[c] / denom);
-#pragma unroll
-                            for (int r = 0; r < R; ++r) {
-                                if (tl.vlo(r)) {
-                                    double q0v = g * pl[r];
-                                    tl.xl[r][c] = tl.xl[r][c] - q0v;
-                                }
-                                if (tl.vhi(r)) {
-                                    double q1v = g * ph[r];
-                                    tl.xh[r][c] = tl.xh[r][c] - q1v;
-                                }
-                            }
-                        }
-                    }
-                }
-            }
-        }
-        if (TMA) {
-            tl.sync();
-            if (producer) mbar_arrive(pp.empty + (int)((k0 + cnt - 1) % S));
-            pp.k = k0 + cnt;
-        }
+        const bool broken = panel_triangle<TMA, S, T, R, C, GEN>(tl, pp, a, denoms, m, col0, p1, q0,
+                                                                 fail, bc, producer);
         if (!broken) tl.store(cols, col0, n + 1);
+#if PDAS_PANEL_TRACE
+        if (trace) {
+            long long t_tri = 0;
+            PANEL_LAP(t_tri);
+            g_panel_trace[0] = t_wait;
+            g_panel_trace[1] = t_apply;
+            g_panel_trace[2] = t_tri;
+            g_panel_trace[3] = (long long)(tile - p0 / C) * C;  // apply steps
+            g_panel_trace[4] = C;                                 // triangle steps
+        }
+#endif
     }
     __threadfence();
     __syncthreads();
@@ -1542,6 +1615,16 @@ static int run_cascade(double* cols, const double* a, const double* d, int m, id
 
 idx_t cascade_flags_count(idx_t m, idx_t n) { return 2 * (n + 2); }  // panel + update flags
 
+#if PDAS_PANEL_TRACE
+}  // namespace pdas
+extern "C" int pdas_debug_panel_trace(long long* host_out) {
+    return cudaMemcpyFromSymbol(host_out, pdas::g_panel_trace, sizeof(pdas::g_panel_trace)) ==
+                   cudaSuccess
+               ? 0
+               : -2;
+}
+namespace pdas {
+#endif
 #if PDAS_WS_TRACE
 }  // namespace pdas
 extern "C" int pdas_debug_ws_trace(long long* host_out) {
