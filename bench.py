@@ -28,6 +28,8 @@ sys.path.insert(0, REPO)
 
 M, N, SEED = 2000, 20000, 0
 METRIC = "PDAS iterations/s (m=2000, n=20000)"
+CONFIG = {"workload": f"c3 dense LP m={M} n={N} seed={SEED} (BASELINE configs[2]), each step = "
+                      "PDAS iteration 1 from the generator's start", "m": M, "n": N}
 UNIT = "iterations/s"
 
 
@@ -175,7 +177,7 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"c3 dense LP m={M} n={N} seed={SEED}", "m": M, "n": N},
+        "config": dict(CONFIG, parallelism=f"CPU, {threads} threads"),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": sample, "sample_seconds": float(np.median(times))},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -337,12 +339,10 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong" if shard else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"c3 dense LP m={M} n={N} seed={SEED} (BASELINE configs[2]), "
-                               "each step = PDAS iteration 1 from the generator's start",
-                   "m": M, "n": N, "l2": "inputs larger than L2 ([Y|x] 320 MB + A + Y)",
-                   "parallelism": (f"column-sharded cascade over {world} GPUs (dist.py)" if shard
-                                   else f"replicas x{world}" if world > 1 else "1 GPU"),
-                   "cascade_block_pivots": 128},
+        "config": dict(CONFIG, l2="inputs larger than L2 ([Y|x] 320 MB + A + Y)",
+                       parallelism=(f"column-sharded cascade over {world} GPUs (dist.py)" if shard
+                                    else f"replicas x{world}" if world > 1 else "1 GPU"),
+                       cascade_block_pivots=128 if shard else 256),
         "e2e": {"value": jobs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,

@@ -47,4 +47,4 @@ for rep in range(args.reps + 1):
         print(f"m={m} n={n} cascade {ms:.2f} ms  {4 * E / ms / 1e9:.2f} TFLOP/s  "
               f"{16 * E / ms / 1e6:.0f} GB/s-equiv  fail={int(fail.item())}  "
               f"variant={os.environ.get('PDAS_CASCADE_VARIANT', '0')} "
-              f"B={os.environ.get('PDAS_CASCADE_BLOCK', '128')}", flush=True)
+              f"B={os.environ.get('PDAS_CASCADE_BLOCK', '256')}", flush=True)
