@@ -484,9 +484,9 @@ __device__ __forceinline__ void apply_impl(Tile<T, R, C, GEN>& tl, Pipe<S>& pp,
                 pipe_issue(pp, use - 1 + S, gc + (size_t)(j - 1 + S) * m,
                            ga + (size_t)(j - 1 + S) * m, m);
         }
+        double g[C];
+        if (active) tl.template finish<true>(part, sden[j], sy[j], g);
         if (active) {
-            double g[C];
-            tl.template finish<true>(part, sden[j], sy[j], g);
             APPLY_LAP(6);  // refill + reduction + B2
             double pl[R], ph[R];
             tl.template load_p<!TMA, FULL>(pc, pl, ph);
