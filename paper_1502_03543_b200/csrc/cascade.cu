@@ -1516,24 +1516,25 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
             cudaStreamWaitEvent(ss.xs, ss.eP, 0);
             update_x(0);
         }
+        auto upd = [&](cudaStream_t s_, idx_t b, idx_t ta, idx_t tb, int* uf, int uc) {
+            if (ta >= tb) return;
+            if (use_ws)
+                kws<<<(unsigned)(tb - ta), kWsThreads, smem_ws, s_>>>(
+                    cols, a, d, denoms, m, n, b * B, blk_end(b), ta, fail, nullptr, uf,
+                    (int)(b + 1), uc);
+            else
+                ku<<<(unsigned)(tb - ta), T * G, smem_u, s_>>>(
+                    cols, a, d, denoms, m, n, b * B, blk_end(b), ta, fail, nullptr, uf,
+                    (int)(b + 1), uc);
+        };
         for (idx_t b = 0; b < nb; ++b) {
             cudaStreamWaitEvent(st, ss.eP, 0);  // panel(b): block b is final
-            // eU marks the START of U(b): panel(b+1) must not be resident (and
-            // spinning on 16-odd SMs) while U(b-1) still runs
+            // eU: the main stream up to U(b-1); panel(b+1) must not be resident
+            // (spinning on its SMs) while U(b-1) still runs
             cudaEventRecord(ss.eU, st);
             const idx_t t0 = b + 1 < nb ? (b + 1) * B / CT : (n + CT - 1) / CT;
             prof.mark(st, 0, b, 0);
-            if (t0 < nt_y) {
-                const int uc = b + 1 < nb ? (int)tiles_of(b + 1) : 0;
-                if (use_ws)
-                    kws<<<(unsigned)(nt_y - t0), kWsThreads, smem_ws, st>>>(
-                        cols, a, d, denoms, m, n, b * B, blk_end(b), t0, fail, nullptr, uflag,
-                        (int)(b + 1), uc);
-                else
-                    ku<<<(unsigned)(nt_y - t0), T * G, smem_u, st>>>(
-                        cols, a, d, denoms, m, n, b * B, blk_end(b), t0, fail, nullptr, uflag,
-                        (int)(b + 1), uc);
-            }
+            upd(st, b, t0, nt_y, uflag, b + 1 < nb ? (int)tiles_of(b + 1) : 0);
             prof.mark(st, 0, b, 1);
             if (b + 1 < nb) {
                 const idx_t p0 = (b + 1) * B;
