@@ -997,18 +997,25 @@ __device__ __forceinline__ void ws_reducer(Pipe<S>& pp, const double* __restrict
 
 // pipe_issue without the empty-barrier protocol (single producer that knows
 // from the named barriers when a stage is free): plain full-barrier refill.
-template <int S, int R, int C>
-__global__ void __launch_bounds__(kWsThreads, 1)
+// TC = 256: one CTA per SM (compute 232 / reducer 40 registers).  TC = 128
+// (m <= 1024: the same 64-double tile per thread with twice the rows): two
+// CTAs per SM, 256 threads each (compute 208 / reducer 48), so the SM
+// interleaves two independent barrier/reduction pipelines.
+template <int S, int R, int C, int TC = kWsT>
+__global__ void __launch_bounds__(TC + 128, TC == 128 ? 2 : 1)
     k_casc_update_ws(double* __restrict__ cols, const double* __restrict__ a,
                      const double* __restrict__ d, const double* __restrict__ denoms, int m,
                      idx_t n, idx_t p0, idx_t p1, idx_t tile0, const int32_t* __restrict__ fail,
                      const int64_t* __restrict__ tiles, int* __restrict__ uflag, int utag,
                      int ucount) {
+    static_assert(TC == 256 || TC == 128, "compute threads");
+    constexpr bool kLdg = (PDAS_WS_LDG && R <= 4) || TC == 128;
+    constexpr int kRegC = TC == 256 ? kWsRegsCompute : 208, kRegR = TC == 256 ? kWsRegsReducer : 48;
     if (*(volatile const int32_t*)fail) return;
     double *red, *bc;
     Pipe<S> pp;
-    carve<kWsT, C, 1, S>(red, bc, pp, false, m);
-    if (!(PDAS_WS_LDG && R <= 4) && threadIdx.x == 0) {
+    carve<TC, C, 1, S>(red, bc, pp, false, m);
+    if (!kLdg && threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) mbar_init(pp.full + s, 1);
         mbar_fence_init();
     }
@@ -1017,31 +1024,31 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     const int cnt = (int)(p1 - p0);
     constexpr int HC = C / 2;
     double* redA = red;
-    double* redB = red + HC * kWsT;
+    double* redB = red + HC * TC;
     double* bcA = bc;
     double* bcB = bc + HC;
-    if (threadIdx.x >= kWsT) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kWsRegsReducer));
-        if constexpr (PDAS_WS_LDG && R <= 4)
-            ws_reducer_ldg<R, C>(pp.sd, pp.sden, pp.sy, cnt, redA, redB, bcA, bcB);
+    if (threadIdx.x >= TC) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegR));
+        if constexpr (kLdg)
+            ws_reducer_ldg<R, C, TC>(pp.sd, pp.sden, pp.sy, cnt, redA, redB, bcA, bcB);
         else
             ws_reducer<S, R, C>(pp, cols, a, p0, cnt, m, redA, redB, bcA, bcB);
         return;
     }
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kWsRegsCompute));
-    Tile<kWsT, R, C, false> tl;
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegC));
+    Tile<TC, R, C, false> tl;
     tl.init(threadIdx.x, m, 0, red, bc);
     const idx_t col0 = (tiles ? tiles[blockIdx.x] : tile0 + blockIdx.x) * C;
     tl.load(cols, col0, n + 1);
     const bool full = __all_sync(0xffffffffu, tl.full());
-    if constexpr (PDAS_WS_LDG && R <= 4) {
+    if constexpr (kLdg) {
         const double* pc = cols + p0 * m;
         const double* ac = a + p0 * m;
         if (full)
-            ws_compute_ldg<R, C, true>(tl, pc, ac, m, pp.sd, cnt, redA, redB, bcA, bcB);
+            ws_compute_ldg<R, C, true, TC>(tl, pc, ac, m, pp.sd, cnt, redA, redB, bcA, bcB);
         else
-            ws_compute_ldg<R, C, false>(tl, pc, ac, m, pp.sd, cnt, redA, redB, bcA, bcB);
-    } else {
+            ws_compute_ldg<R, C, false, TC>(tl, pc, ac, m, pp.sd, cnt, redA, redB, bcA, bcB);
+    } else if constexpr (TC == 256) {
         if (full)
             ws_compute<S, R, C, true>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
         else
@@ -1050,7 +1057,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     tl.store(cols, col0, n + 1);
     if (uflag && (int)blockIdx.x < ucount) {  // tile done: the next panel may take it
         __threadfence();
-        named_bar(5, kWsT);
+        named_bar(5, TC);
         if (threadIdx.x == 0) st_release(uflag + col0 / C, utag);
     }
 }
@@ -1310,7 +1317,10 @@ static CascCfg cascade_cfg(idx_t m) {
     if (H == 64) return {64, 1, 8, 1, 8};
     if (H == 128) return {128, 1, 8, 1, 8};
     if (H == 256) return {256, 1, 8, 2, 16};
-    if (H == 512) return variant == 1 ? CascCfg{256, 2, 8, 2, 16} : CascCfg{256, 2, 16, 1, 16};
+    if (H == 512)
+        return variant == 1   ? CascCfg{256, 2, 8, 2, 16}
+               : variant == 2 ? CascCfg{256, 2, 16, 1, 16}
+                              : CascCfg{128, 4, 8, 1, 8};  // 2 WS CTAs per SM
     if (H == 1024) return variant == 1 ? CascCfg{256, 4, 4, 2, 8} : CascCfg{256, 4, 8, 1, 8};
     if (H == 2048) return {256, 8, 4, 1, 4};
     if (H == 4096) return {256, 16, 2, 1, 2};
@@ -1436,11 +1446,15 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
     cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
     // warp-specialized update for the 256-thread single-group layouts
     // (R >= 16 spills the compute warpgroups' 232-register budget)
-    constexpr bool kUseWs = TMA && T == kWsT && G == 1 && CT % 2 == 0 && S >= 2 && R <= 8;
+    constexpr bool kWs256 = TMA && T == kWsT && G == 1 && CT % 2 == 0 && S >= 2 && R <= 8;
+    constexpr bool kWs128 = T == 128 && G == 1 && CT % 2 == 0 && R >= 2 && R <= 4;
+    constexpr bool kUseWs = kWs256 || kWs128;
     constexpr int CW = kUseWs ? CT : 2;
     constexpr int RW = kUseWs ? R : 1;
-    auto kws = k_casc_update_ws<S, RW, CW>;
-    const size_t smem_ws = casc_smem_bytes<kWsT, CW, 1>(S, m);
+    constexpr int TCW = kWs128 ? 128 : kWsT;
+    const int ws_threads = TCW + 128;
+    auto kws = k_casc_update_ws<S, RW, CW, TCW>;
+    const size_t smem_ws = casc_smem_bytes<TCW, CW, 1>(S, m);
     const bool use_ws = kUseWs && env_int("PDAS_CASCADE_WS", 1) != 0;
     if (use_ws)
         cudaFuncSetAttribute(kws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ws);
@@ -1455,7 +1469,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         if (op.p1 - op.p0 > kMaxBlock || op.p1 <= op.p0) return PDAS_ERR_ARG;
         if (op.ntiles > 0) {
             if (use_ws)
-                kws<<<(unsigned)op.ntiles, kWsThreads, smem_ws, st>>>(
+                kws<<<(unsigned)op.ntiles, ws_threads, smem_ws, st>>>(
                     cols, a, d, denoms, m, n, op.p0, op.p1, 0, fail, op.tiles, nullptr, 0, 0);
             else
                 ku<<<(unsigned)op.ntiles, T * G, smem_u, st>>>(cols, a, d, denoms, m, n, op.p0,
@@ -1470,7 +1484,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         if (t0 >= ntiles) return;
         const int uc = uf && b + 1 < nb ? (int)tiles_of(b + 1) : 0;
         if (use_ws)
-            kws<<<(unsigned)(ntiles - t0), kWsThreads, smem_ws, st>>>(
+            kws<<<(unsigned)(ntiles - t0), ws_threads, smem_ws, st>>>(
                 cols, a, d, denoms, m, n, b * B, blk_end(b), t0, fail, nullptr, uf, (int)(b + 1), uc);
         else
             ku<<<(unsigned)(ntiles - t0), T * G, smem_u, st>>>(
@@ -1491,7 +1505,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         const idx_t nt_y = xlane ? ntiles - 1 : ntiles;  // tiles U(b) covers
         auto update_x = [&](idx_t b) {  // block b -> the x tile (1 CTA)
             if (use_ws)
-                kws<<<1, kWsThreads, smem_ws, ss.xs>>>(cols, a, d, denoms, m, n, b * B, blk_end(b),
+                kws<<<1, ws_threads, smem_ws, ss.xs>>>(cols, a, d, denoms, m, n, b * B, blk_end(b),
                                                        ntiles - 1, fail, nullptr, nullptr, 0, 0);
             else
                 ku<<<1, T * G, smem_u, ss.xs>>>(cols, a, d, denoms, m, n, b * B, blk_end(b),
@@ -1519,7 +1533,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         auto upd = [&](cudaStream_t s_, idx_t b, idx_t ta, idx_t tb, int* uf, int uc) {
             if (ta >= tb) return;
             if (use_ws)
-                kws<<<(unsigned)(tb - ta), kWsThreads, smem_ws, s_>>>(
+                kws<<<(unsigned)(tb - ta), ws_threads, smem_ws, s_>>>(
                     cols, a, d, denoms, m, n, b * B, blk_end(b), ta, fail, nullptr, uf,
                     (int)(b + 1), uc);
             else
@@ -1650,6 +1664,7 @@ static int dispatch_cascade(double* cols, const double* a, const double* d, idx_
     PDAS_CASC(32, 1, 8, 1, 8)
     PDAS_CASC(64, 1, 8, 1, 8)
     PDAS_CASC(128, 1, 8, 1, 8)
+    PDAS_CASC(128, 4, 8, 1, 8)
     PDAS_CASC(256, 1, 8, 2, 16)
     PDAS_CASC(256, 2, 8, 2, 16)
     PDAS_CASC(256, 4, 8, 1, 8)
