@@ -1316,7 +1316,8 @@ static CascCfg cascade_cfg(idx_t m) {
     if (H <= 32) return {32, 1, 8, 1, 8};
     if (H == 64) return {64, 1, 8, 1, 8};
     if (H == 128) return {128, 1, 8, 1, 8};
-    if (H == 256) return {256, 1, 8, 2, 16};
+    if (H == 256)  // 2 WS CTAs per SM; variant 3: the 512-thread ping-pong layout
+        return variant == 3 ? CascCfg{256, 1, 8, 2, 16} : CascCfg{128, 2, 8, 1, 8};
     if (H == 512)
         return variant == 1   ? CascCfg{256, 2, 8, 2, 16}
                : variant == 2 ? CascCfg{256, 2, 16, 1, 16}
@@ -1665,6 +1666,7 @@ static int dispatch_cascade(double* cols, const double* a, const double* d, idx_
     PDAS_CASC(64, 1, 8, 1, 8)
     PDAS_CASC(128, 1, 8, 1, 8)
     PDAS_CASC(128, 4, 8, 1, 8)
+    PDAS_CASC(128, 2, 8, 1, 8)
     PDAS_CASC(256, 1, 8, 2, 16)
     PDAS_CASC(256, 2, 8, 2, 16)
     PDAS_CASC(256, 4, 8, 1, 8)
