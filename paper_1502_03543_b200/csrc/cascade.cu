@@ -650,11 +650,11 @@ __device__ long long g_ws_trace[2][kMaxBlock][6];
     } while (0)
 #endif
 
-template <int S, int R, int C, bool FULL>
-__device__ __forceinline__ void ws_compute(Tile<kWsT, R, C, false>& tl, const double* buf, int mp,
+template <int S, int R, int C, bool FULL, int TC = kWsT>
+__device__ __forceinline__ void ws_compute(Tile<TC, R, C, false>& tl, const double* buf, int mp,
                                            const double* sd, int cnt, double* redA, double* redB,
                                            const double* bcA, const double* bcB) {
-    constexpr int HC = C / 2, NT = kWsThreads;
+    constexpr int HC = C / 2, NT = TC + 128;
     const int stage = 2 * mp;
     double vl[R], vh[R], pl[R], ph[R];
     auto sptr = [&](int j) -> const double* { return buf + (j % S) * stage; };
@@ -669,7 +669,7 @@ __device__ __forceinline__ void ws_compute(Tile<kWsT, R, C, false>& tl, const do
                 double hi = vh[r] * tl.xh[r][h0 + c];
                 s[r] = lo + hi;
             }
-            red[c * kWsT + tl.t] = lane_tree<R>(s);
+            red[c * TC + tl.t] = lane_tree<R>(s);
         }
     };
     auto axpy = [&](int h0, const double* bc) {
@@ -908,13 +908,14 @@ __device__ __forceinline__ void ws_reducer_ldg(const double* sd, const double* s
     named_bar(1, NT);  // the compute warps' final PA arrival
 }
 
-template <int S, int R, int C>
+template <int S, int R, int C, int TC = kWsT>
 __device__ __forceinline__ void ws_reducer(Pipe<S>& pp, const double* __restrict__ cols,
                                            const double* __restrict__ a, idx_t p0, int cnt, int m,
                                            const double* redA, const double* redB, double* bcA,
                                            double* bcB) {
-    constexpr int HC = C / 2, NT = kWsThreads, NW = kWsT / 32;
-    const int rt = threadIdx.x - kWsT;  // 0..127
+    constexpr int HC = C / 2, NT = TC + 128, NW = TC / 32;
+    constexpr bool kLateIssue = PDAS_ISSUE_LATE && S >= 3;
+    const int rt = threadIdx.x - TC;  // 0..127
     const int w = rt >> 5, lane = rt & 31;
     const bool producer = rt == 0;
     const double* sd = pp.sd;
@@ -933,7 +934,7 @@ __device__ __forceinline__ void ws_reducer(Pipe<S>& pp, const double* __restrict
             if (c < HC) {
                 double q[NW];
 #pragma unroll
-                for (int i = 0; i < NW; ++i) q[i] = red[c * kWsT + lane + 32 * i];
+                for (int i = 0; i < NW; ++i) q[i] = red[c * TC + lane + 32 * i];
                 v[k] = lane_tree<NW>(q);
             }
         }
@@ -966,7 +967,9 @@ __device__ __forceinline__ void ws_reducer(Pipe<S>& pp, const double* __restrict
         WS_MARK(1, j, 0);
         named_bar(1, NT);  // partials A(j) published (C2(j-1) done: stage j-1 free)
         WS_MARK(1, j, 1);
-        if (!PDAS_ISSUE_LATE && j >= 1 && producer && j - 1 + S < cnt)
+        // S = 2: stage j+1 is the one C2(j-1) just released -- refill it now,
+        // before waiting on it below (the late refill would deadlock)
+        if (!kLateIssue && j >= 1 && producer && j - 1 + S < cnt)
             pipe_issue(pp, j - 1 + S, cols + (p0 + j - 1 + S) * m, a + (p0 + j - 1 + S) * m, m,
                        false);
         if (act) reduce(redA, bcA, den, y);
@@ -979,7 +982,7 @@ __device__ __forceinline__ void ws_reducer(Pipe<S>& pp, const double* __restrict
         named_arrive(3, NT);
         WS_MARK(1, j, 3);
         // refill the stage C2(j-1) released, after gA(j) is out
-        if (PDAS_ISSUE_LATE && j >= 1 && producer && j - 1 + S < cnt)
+        if (kLateIssue && j >= 1 && producer && j - 1 + S < cnt)
             pipe_issue(pp, j - 1 + S, cols + (p0 + j - 1 + S) * m, a + (p0 + j - 1 + S) * m, m,
                        false);
         // ---- R2(j)
@@ -1009,8 +1012,9 @@ __global__ void __launch_bounds__(TC + 128, TC == 128 ? 2 : 1)
                      const int64_t* __restrict__ tiles, int* __restrict__ uflag, int utag,
                      int ucount) {
     static_assert(TC == 256 || TC == 128, "compute threads");
-    constexpr bool kLdg = (PDAS_WS_LDG && R <= 4) || TC == 128;
-    constexpr int kRegC = TC == 256 ? kWsRegsCompute : 208, kRegR = TC == 256 ? kWsRegsReducer : 48;
+    constexpr bool kLdg = PDAS_WS_LDG && R <= 4;
+    constexpr int kRegC = TC == 256 ? kWsRegsCompute : (kLdg ? 208 : 216);
+    constexpr int kRegR = TC == 256 ? kWsRegsReducer : (kLdg ? 48 : 40);
     if (*(volatile const int32_t*)fail) return;
     double *red, *bc;
     Pipe<S> pp;
@@ -1032,7 +1036,7 @@ __global__ void __launch_bounds__(TC + 128, TC == 128 ? 2 : 1)
         if constexpr (kLdg)
             ws_reducer_ldg<R, C, TC>(pp.sd, pp.sden, pp.sy, cnt, redA, redB, bcA, bcB);
         else
-            ws_reducer<S, R, C>(pp, cols, a, p0, cnt, m, redA, redB, bcA, bcB);
+            ws_reducer<S, R, C, TC>(pp, cols, a, p0, cnt, m, redA, redB, bcA, bcB);
         return;
     }
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegC));
@@ -1048,11 +1052,11 @@ __global__ void __launch_bounds__(TC + 128, TC == 128 ? 2 : 1)
             ws_compute_ldg<R, C, true, TC>(tl, pc, ac, m, pp.sd, cnt, redA, redB, bcA, bcB);
         else
             ws_compute_ldg<R, C, false, TC>(tl, pc, ac, m, pp.sd, cnt, redA, redB, bcA, bcB);
-    } else if constexpr (TC == 256) {
+    } else {
         if (full)
-            ws_compute<S, R, C, true>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
+            ws_compute<S, R, C, true, TC>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
         else
-            ws_compute<S, R, C, false>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
+            ws_compute<S, R, C, false, TC>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
     }
     tl.store(cols, col0, n + 1);
     if (uflag && (int)blockIdx.x < ucount) {  // tile done: the next panel may take it
@@ -1448,7 +1452,8 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
     // warp-specialized update for the 256-thread single-group layouts
     // (R >= 16 spills the compute warpgroups' 232-register budget)
     constexpr bool kWs256 = TMA && T == kWsT && G == 1 && CT % 2 == 0 && S >= 2 && R <= 8;
-    constexpr bool kWs128 = T == 128 && G == 1 && CT % 2 == 0 && R >= 2 && R <= 4;
+    constexpr bool kWs128 = T == 128 && G == 1 && CT % 2 == 0 && R >= 2 &&
+                            (R <= 4 || (TMA && R <= 8 && S >= 2 && S <= 3));
     constexpr bool kUseWs = kWs256 || kWs128;
     constexpr int CW = kUseWs ? CT : 2;
     constexpr int RW = kUseWs ? R : 1;
@@ -1609,9 +1614,10 @@ static int run_cascade(double* cols, const double* a, const double* d, int m, id
     // TMA pivot staging pays off only for the 256-thread tiles (m > 256); for
     // smaller m the per-pivot bulk-copy + mbarrier round trip dominates the
     // step (measured 3-5x slower than direct L2 loads at m = 50 / 64).
-    const bool aligned = T == 256 && (m % 2 == 0) &&
+    const bool aligned = (T == 256 || (T == 128 && R == 8)) && (m % 2 == 0) &&
                          (((uintptr_t)cols | (uintptr_t)a) % 16 == 0);
-    const size_t budget = 210 * 1024;
+    // two warp-specialized CTAs per SM for the 128-thread layouts
+    const size_t budget = (T == 128 ? 110 : 210) * 1024;
     if (aligned && env_int("PDAS_CASCADE_STAGES", 5) >= 5 &&
         casc_smem_bytes<T, CT, 1>(5, m) <= budget &&
         casc_smem_bytes<T, Cu, G>(5, m) <= budget)
@@ -1620,6 +1626,10 @@ static int run_cascade(double* cols, const double* a, const double* d, int m, id
     if (aligned && casc_smem_bytes<T, CT, 1>(4, m) <= budget &&
         casc_smem_bytes<T, Cu, G>(4, m) <= budget)
         return run_cascade_impl<true, 4, T, R, Cu, G, CT>(cols, a, d, m, n, denoms, fail, flags,
+                                                          epoch, B, st, op);
+    if (T == 128 && aligned && casc_smem_bytes<T, CT, 1>(3, m) <= budget &&
+        casc_smem_bytes<T, Cu, G>(3, m) <= budget)
+        return run_cascade_impl<true, 3, T, R, Cu, G, CT>(cols, a, d, m, n, denoms, fail, flags,
                                                           epoch, B, st, op);
     if (aligned && casc_smem_bytes<T, CT, 1>(2, m) <= budget &&
         casc_smem_bytes<T, Cu, G>(2, m) <= budget)

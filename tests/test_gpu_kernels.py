@@ -233,3 +233,28 @@ def test_cascade_with_fused_x0(gpu, m, n):
     assert int(fail.item()) == ret
     if ret == 0:
         assert bits_equal(dv.download(cols).reshape((m, n + 1), order="F"), cref)
+
+
+@pytest.mark.parametrize("m", [3000, 3500, 4096, 5000])
+def test_cascade_large_m_vs_oracle(gpu, m):
+    """m > 2048: the 2- and 4-stage TMA rings (the 5-stage one no longer fits
+    shared memory) and the R >= 8 tiles; random [Y | x] (no basis needed)."""
+    n = 300
+    rng = np.random.default_rng(m)
+    a = np.asfortranarray(rng.uniform(-1, 1, (m, n)))
+    d = np.power(10.0, rng.uniform(-2, 2, n))
+    d[rng.random(n) < 0.1] = 1.0
+    cols = np.asfortranarray(rng.uniform(-1, 1, (m, n + 1)) / np.sqrt(m))
+    ref = cols.copy(order="F")
+    ret = O.restated().solve_sweeps(ref, a, d, np.zeros(n + 1), np.zeros(m), 8)
+    got = cols.copy(order="F")
+    assert K_solve(gpu, got, a, d) == ret
+    if ret == 0:
+        assert bits_equal(got, ref)
+
+
+def K_solve(gpu, cols, a, d):
+    from paper_1502_03543_b200._core import kernels
+
+    m, n = a.shape
+    return kernels.solve_sweeps(cols, a, d, np.zeros(n + 1), np.zeros(m), 1)
