@@ -143,11 +143,12 @@ struct Tile {
         }
     }
 
-    __device__ __forceinline__ void store(double* __restrict__ cols, idx_t col0, idx_t ncols) const {
+    __device__ __forceinline__ void store(double* __restrict__ cols, idx_t col0, idx_t ncols,
+                                          int c_lo = 0, int c_hi = C) const {
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             const idx_t col = col0 + c;
-            if (col >= ncols) continue;
+            if (c < c_lo || c >= c_hi || col >= ncols) continue;
             double* p = cols + col * m;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -314,6 +315,11 @@ struct Tile {
 // `k` counts stage uses (identical in every thread of the CTA).  S (stage
 // count) is a compile-time constant so stage arithmetic is shifts/masks.
 constexpr int kMaxBlock = 256;  // pivots per block (B) upper bound
+#ifndef PDAS_PANEL_CHUNKS
+#define PDAS_PANEL_CHUNKS 2
+#endif
+// a panel tile publishes its final columns in this many chunks (flags per chunk)
+constexpr int kPanelChunks = PDAS_PANEL_CHUNKS;
 constexpr int kDefaultBlock = 256;  // 1-GPU default (c3: 2% faster than 128; dist uses 128)
 
 template <int S>
@@ -1119,7 +1125,9 @@ __device__ __forceinline__ bool panel_triangle(Tile<T, R, C, GEN>& tl, Pipe<S>& 
                                                const double* __restrict__ a,
                                                double* __restrict__ denoms, int m, idx_t col0,
                                                idx_t p1, idx_t q0, int32_t* __restrict__ fail,
-                                               double* bc, bool producer) {
+                                               double* bc, bool producer,
+                                               double* __restrict__ cols = nullptr, idx_t n = 0,
+                                               int* __restrict__ cflags = nullptr, int epoch = 0) {
     // triangle over this tile's own pivot columns, A columns via the pipe
     const int cnt = (int)((col0 + C < p1 ? col0 + C : p1) - col0);
     const unsigned k0 = pp.k;
@@ -1194,6 +1202,15 @@ __device__ __forceinline__ bool panel_triangle(Tile<T, R, C, GEN>& tl, Pipe<S>& 
                     }
                 }
             }
+            // end of a chunk: its columns are final -- store and publish them so
+            // the next tile's CTA starts on them while this triangle goes on
+            constexpr int CH = C / kPanelChunks > 0 ? C / kPanelChunks : 1;
+            if (cflags && (cl + 1) % CH == 0 && cl + 1 < C && cl + 1 < cnt && !broken) {
+                tl.store(cols, col0, n + 1, cl + 1 - CH, cl + 1);
+                __threadfence();
+                tl.sync();
+                if (producer) st_release(cflags + (cl + 1) / CH - 1, epoch);
+            }
         }
     }
     if (TMA) {
@@ -1216,8 +1233,12 @@ __global__ void __launch_bounds__(T, 1)
                  idx_t q0, idx_t p0, idx_t p1, int32_t* __restrict__ fail, int* __restrict__ flags,
                  int epoch, const int* __restrict__ uflag, int utag) {
     const idx_t tile = p0 / C + blockIdx.x;
+    // a tile's final columns are published in NCH chunks of CH (flags[tile*NCH + ch])
+    constexpr int CH = C / kPanelChunks > 0 ? C / kPanelChunks : 1;
+    constexpr int NCH = C / CH;
     if (*(volatile int32_t*)fail) {  // still publish: later tiles may be waiting
-        if (threadIdx.x == 0) st_release(flags + tile, epoch);
+        if (threadIdx.x == 0)
+            for (int ch = 0; ch < NCH; ++ch) st_release(flags + tile * NCH + ch, epoch);
         return;
     }
     double *red, *bc;
@@ -1264,28 +1285,37 @@ __global__ void __launch_bounds__(T, 1)
     } while (0)
 #endif
     for (idx_t tp = p0 / C; tp < tile && !dead; ++tp) {
-        if (producer)
-            while (ld_acquire(flags + tp) != epoch) __nanosleep(32);
-        __syncthreads();
-        PANEL_LAP(t_wait);
-        if (*(volatile int32_t*)fail) {
-            dead = true;
-            break;
+        // the previous tile chunk by chunk (its triangle is still running);
+        // older tiles are complete: one wait on their last chunk
+        const bool prev = tp == tile - 1;
+        for (int ch = prev ? 0 : NCH - 1; ch < NCH; ++ch) {
+            if (producer)
+                while (ld_acquire(flags + tp * NCH + ch) != epoch) __nanosleep(32);
+            __syncthreads();
+            PANEL_LAP(t_wait);
+            if (*(volatile int32_t*)fail) {
+                dead = true;
+                break;
+            }
+            const idx_t pa = tp * C + (prev ? ch * CH : 0);
+            const idx_t pe = tp * C + (ch + 1) * CH;
+            const idx_t pb = pe < p1 ? pe : p1;
+            if (pa >= pb) continue;
+            if (threadIdx.x < pb - pa) {
+                const double den = __ldcg(denoms + pa + threadIdx.x);
+                pp.sden[pa + threadIdx.x - q0] = den;
+                pp.sy[pa + threadIdx.x - q0] = div_recip(den);
+            }
+            fence_proxy_async_global();  // peer CTA's generic stores -> our TMA reads
+            __syncthreads();
+            apply_global<TMA>(tl, pp, cols, a, q0, pa, pb, producer);
+            PANEL_LAP(t_apply);
         }
-        const idx_t e = tp * C + C < p1 ? tp * C + C : p1;
-        if (threadIdx.x < C && tp * C + threadIdx.x < e) {
-            const double den = __ldcg(denoms + tp * C + threadIdx.x);
-            pp.sden[tp * C + threadIdx.x - q0] = den;
-            pp.sy[tp * C + threadIdx.x - q0] = div_recip(den);
-        }
-        fence_proxy_async_global();  // peer CTA's generic stores -> our TMA reads
-        __syncthreads();
-        apply_global<TMA>(tl, pp, cols, a, q0, tp * C, e, producer);
-        PANEL_LAP(t_apply);
     }
     if (!dead) {
-        const bool broken = panel_triangle<TMA, S, T, R, C, GEN>(tl, pp, a, denoms, m, col0, p1, q0,
-                                                                 fail, bc, producer);
+        const bool broken = panel_triangle<TMA, S, T, R, C, GEN>(
+            tl, pp, a, denoms, m, col0, p1, q0, fail, bc, producer, cols, n,
+            NCH > 1 ? flags + tile * NCH : nullptr, epoch);
         if (!broken) tl.store(cols, col0, n + 1);
 #if PDAS_PANEL_TRACE
         if (trace) {
@@ -1301,7 +1331,8 @@ __global__ void __launch_bounds__(T, 1)
     }
     __threadfence();
     __syncthreads();
-    if (producer) st_release(flags + tile, epoch);
+    if (producer)
+        for (int ch = 0; ch < NCH; ++ch) st_release(flags + tile * NCH + ch, epoch);
 }
 
 // ------------------------------------------------------------ host side
