@@ -17,12 +17,14 @@ PCIe bus per iteration; the SingularUpdate fallback to the direct solve
 
 from __future__ import annotations
 
+import os
 import time
 
 import numpy as np
 
 from . import _device as dv
 from ._lib import (
+    load,
     OFF_CASCADE_FAIL,
     OFF_CHOL_FAIL,
     STATE_BYTES,
@@ -167,8 +169,6 @@ class DeviceSolver:
         if backend == "woodbury":
             self.basis = basis or prepare_basis(prob, L0)
             self.cols = dv.empty(m * (n + 1))
-            from ._lib import load
-
             self.casc_ws = t.zeros(int(load().pdas_cascade_ws_bytes(m, n)), dtype=t.uint8,
                                    device=dv.device())
             self.epoch = 0
@@ -252,7 +252,10 @@ class DeviceSolver:
         call("pdas_solve_sweeps_ws_x0", dv.ptr(self.cols), dv.ptr(self.prob.A), dv.ptr(self.d),
              dv.ptr(self.basis.L0), m, n, dv.ptr(self.casc_ws), self.epoch,
              self._sptr(OFF_CASCADE_FAIL), dv.stream())
-        self.launches += 2 + 3 * ((n + 127) // 128)
+        # x0 solve (2) + per pivot block: panel, update, and the x lane's update
+        blk = int(os.environ.get("PDAS_CASCADE_BLOCK", "256"))
+        xlane = n % int(load().pdas_cascade_tile_width(m)) == 0
+        self.launches += 2 + (3 if xlane else 2) * ((n + blk - 1) // blk)
 
     def enqueue_solve(self) -> None:
         """Scaling, rhs and the normal-equations solve (cascade or direct)."""
