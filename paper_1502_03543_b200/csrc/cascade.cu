@@ -634,7 +634,10 @@ constexpr int kWsThreads = 384; // + reducer warpgroup
 #ifndef PDAS_WS_REGS_R
 #define PDAS_WS_REGS_R 40
 #endif
-constexpr int kWsRegsCompute = 232, kWsRegsReducer = PDAS_WS_REGS_R;
+#ifndef PDAS_WS_REGS_C
+#define PDAS_WS_REGS_C 232
+#endif
+constexpr int kWsRegsCompute = PDAS_WS_REGS_C, kWsRegsReducer = PDAS_WS_REGS_R;
 
 // Diagnostic build only (make variant VDEFS=-DPDAS_WS_TRACE=1): clock64 marks
 // of compute thread 0 / reducer thread 0 of one CTA per pivot, read back with
