@@ -35,14 +35,15 @@ fail = torch.zeros(1, dtype=torch.int32, device="cuda")
 call("pdas_solve_sweeps_ws", dv.ptr(cols), dv.ptr(A), dv.ptr(d), m, n, dv.ptr(ws), 1,
      dv.ptr(fail), torch.cuda.current_stream().cuda_stream)
 torch.cuda.synchronize()
-buf = (ctypes.c_longlong * (2 * 128 * 6))()
+KB = 256  # kMaxBlock in cascade.cu (trace rows per role)
+buf = (ctypes.c_longlong * (2 * KB * 6))()
 lib = load()
 lib.pdas_debug_ws_trace.argtypes = [ctypes.c_void_p]
 assert lib.pdas_debug_ws_trace(ctypes.addressof(buf)) == 0
-t = np.frombuffer(buf, dtype=np.int64).reshape(2, 128, 6).astype(np.float64)
+t = np.frombuffer(buf, dtype=np.int64).reshape(2, KB, 6).astype(np.float64)
 C, Rd = t[0], t[1]
 rows = []
-for j in range(1, 127):
+for j in range(1, KB - 2):
     c1 = C[j, 2] - C[j, 1]           # after GB -> after PB arrive
     wga = C[j, 3] - C[j, 2]          # waiting for GA
     c2 = C[j, 4] - C[j, 3]           # C2 work
@@ -57,6 +58,6 @@ for j in range(1, 127):
 a = np.array(rows)
 names = ["period", "C1", "wait GA", "C2", "wait GB", "R wait PA", "R1", "stage wait",
          "R wait PB", "R2"]
-print(f"m={m} n={n}: median cycles per pivot over pivots 1..126 of one CTA's last update")
+print(f"m={m} n={n}: median cycles per pivot over pivots 1..{KB - 3} of one CTA's last update")
 for k, nm in enumerate(names):
     print(f"  {nm:11s} median {np.median(a[:, k]):8.0f}   p90 {np.percentile(a[:, k], 90):8.0f}")
