@@ -212,7 +212,7 @@ def run_ours(args):
     if shard:
         from paper_1502_03543_b200.dist import ShardedSolver
 
-        eng = ShardedSolver(prob, dist.group.WORLD, 0.9, L0=L0)
+        eng = ShardedSolver(prob, dist.group.WORLD, 0.9, L0=L0, exchange=args.exchange)
     else:
         eng = DeviceSolver(prob, "woodbury", 0.9, L0=L0)
     torch.cuda.synchronize()
@@ -340,7 +340,8 @@ def run_ours(args):
         "scaling": "strong" if shard else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": dict(CONFIG, l2="inputs larger than L2 ([Y|x] 320 MB + A + Y)",
-                       parallelism=(f"column-sharded cascade over {world} GPUs (dist.py)" if shard
+                       parallelism=(f"column-sharded cascade over {world} GPUs (dist.py, "
+                                    f"{args.exchange} block exchange)" if shard
                                     else f"replicas x{world}" if world > 1 else "1 GPU"),
                        cascade_block_pivots=128 if shard else 256),
         "e2e": {"value": jobs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
@@ -379,6 +380,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--mode", default="shard", choices=["shard", "replicas"],
                     help="N>1: one LP column-sharded over the GPUs, or N independent LPs")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+                    help="shard mode: NCCL broadcast per pivot block, or the panel's fused "
+                         "NVLink peer stores")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

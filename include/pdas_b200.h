@@ -152,6 +152,26 @@ int pdas_cascade_update(double* cols, const double* a, const double* d, int64_t 
                         int64_t p0, int64_t p1, const int64_t* tiles_dev, int64_t ntiles,
                         void* ws, int32_t* fail_dev, void* stream);
 
+/* The block exchange of the sharded cascade fused into the panel (SURVEY.md
+ * §8(e): the pivot owner's finished columns go to every peer by in-kernel
+ * NVLink stores instead of an NCCL broadcast per block; replaces the
+ * torch.distributed.broadcast calls of dist.run_collective, which stand where
+ * the reference's thread pool shares one address space, parallel.py:169-209).
+ * panel_peers: pdas_cascade_panel, plus each panel tile stores its final
+ * columns from registers into every peer's cols, its denominators into the
+ * peer's ws, a breakdown into the peer's fail word, then releases a
+ * system-scope flag per tile in the peer's ws.  peer_cols / peer_ws /
+ * peer_fail: HOST arrays of npeers (<= 7) device addresses valid in this
+ * process (CUDA IPC / symmetric-memory peer mappings).
+ * peer_wait: on a non-owner, block the stream until every tile covering
+ * columns [c0, c1) has been released for `epoch` (traps after 30 s). */
+int pdas_cascade_panel_peers(double* cols, const double* a, const double* d, int64_t m, int64_t n,
+                             int64_t q0, int64_t p0, int64_t p1, void* ws, int32_t epoch,
+                             int32_t* fail_dev, int32_t npeers, const uint64_t* peer_cols,
+                             const uint64_t* peer_ws, const uint64_t* peer_fail, void* stream);
+int pdas_cascade_peer_wait(void* ws, int64_t m, int64_t n, int64_t c0, int64_t c1, int32_t epoch,
+                           void* stream);
+
 /* cholesky_solve (linalg.py:126-132) for ONE right-hand side, in place on
  * x (m): the per-iteration x0 = L0^-T L0^-1 (A x) of init_workspace
  * (normal.py:123).  Same rounding sequence as cholesky_solve_many with k=1,

@@ -251,6 +251,52 @@ int pdas_cascade_panel(double* cols, const double* a, const double* d, int64_t m
                       "cascade_panel");
 }
 
+int pdas_cascade_panel_peers(double* cols, const double* a, const double* d, int64_t m, int64_t n,
+                             int64_t q0, int64_t p0, int64_t p1, void* ws, int32_t epoch,
+                             int32_t* fail_dev, int32_t npeers, const uint64_t* peer_cols,
+                             const uint64_t* peer_ws, const uint64_t* peer_fail, void* stream) {
+    if (m < 1 || n < 1 || fail_dev == nullptr || ws == nullptr || epoch < 1 || npeers < 0 ||
+        npeers > pdas::kMaxPeers ||
+        (npeers > 0 && (peer_cols == nullptr || peer_ws == nullptr || peer_fail == nullptr)))
+        return set_err(PDAS_ERR_ARG, "cascade_panel_peers: bad args");
+    if (m > pdas::cascade_supported_m())
+        return set_err(PDAS_ERR_UNSUPPORTED,
+                       "cascade_panel_peers: m above the compiled configurations");
+    const int ct = pdas::cascade_tile_width(m);
+    if (q0 < 0 || q0 > p0 || p0 >= p1 || p1 > n || p0 % ct != 0 || q0 % ct != 0 ||
+        p1 - p0 > pdas::kCascadeBlock || p0 - q0 > pdas::kCascadeBlock)
+        return set_err(PDAS_ERR_ARG, "cascade_panel_peers: block bounds");
+    double* denoms;
+    int* flags;
+    split_ws(ws, n, &denoms, &flags);
+    double* pc[pdas::kMaxPeers];
+    double* pd[pdas::kMaxPeers];
+    int32_t* pf[pdas::kMaxPeers];
+    int* pg[pdas::kMaxPeers];
+    for (int q = 0; q < npeers; ++q) {
+        pc[q] = reinterpret_cast<double*>(peer_cols[q]);
+        pf[q] = reinterpret_cast<int32_t*>(peer_fail[q]);
+        split_ws(reinterpret_cast<void*>(peer_ws[q]), n, &pd[q], &pg[q]);
+    }
+    return check_cuda(pdas::launch_cascade_panel_peers(cols, a, d, m, n, q0, p0, p1, denoms,
+                                                       fail_dev, flags, epoch, npeers, pc, pd, pf,
+                                                       pg, S(stream)),
+                      "cascade_panel_peers");
+}
+
+int pdas_cascade_peer_wait(void* ws, int64_t m, int64_t n, int64_t c0, int64_t c1, int32_t epoch,
+                           void* stream) {
+    if (m < 1 || n < 1 || ws == nullptr || epoch < 1 || c0 < 0 || c1 < c0 || c1 > n + 1)
+        return set_err(PDAS_ERR_ARG, "cascade_peer_wait: bad args");
+    if (m > pdas::cascade_supported_m())
+        return set_err(PDAS_ERR_UNSUPPORTED, "cascade_peer_wait: m above the compiled configurations");
+    double* denoms;
+    int* flags;
+    split_ws(ws, n, &denoms, &flags);
+    return check_cuda(pdas::launch_peer_wait(flags, m, c0, c1, epoch, S(stream)),
+                      "cascade_peer_wait");
+}
+
 int pdas_cascade_update(double* cols, const double* a, const double* d, int64_t m, int64_t n,
                         int64_t p0, int64_t p1, const int64_t* tiles_dev, int64_t ntiles,
                         void* ws, int32_t* fail_dev, void* stream) {

@@ -80,6 +80,22 @@ __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ void st_release_sys(int* p, int v) {
+    asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+    int v;
+    asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -321,6 +337,29 @@ constexpr int kMaxBlock = 256;  // pivots per block (B) upper bound
 // a panel tile publishes its final columns in this many chunks (flags per chunk)
 constexpr int kPanelChunks = PDAS_PANEL_CHUNKS;
 constexpr int kDefaultBlock = 256;  // 1-GPU default (c3: 2% faster than 128; dist uses 128)
+
+// Peers of a column-sharded cascade (dist.py): device addresses, valid in
+// this process (NVLink peer mappings), of every other rank's [Y|x], cascade
+// denominators, fail word and panel flags.  count = 0: single GPU.
+struct PeerSet {
+    int count;
+    double* cols[kMaxPeers];
+    double* denoms[kMaxPeers];
+    int32_t* fail[kMaxPeers];
+    int* flags[kMaxPeers];
+};
+
+// Publish a breakdown to the peers (before their flag), then release the
+// tile's flag on every peer (system scope: the stores went over NVLink).
+__device__ __forceinline__ void peer_signal(const PeerSet& peers, const int32_t* fail,
+                                            const int* flags, idx_t flag_idx, int epoch) {
+    (void)flags;
+    const int32_t f = *(volatile const int32_t*)fail;
+    if (f)
+        for (int q = 0; q < peers.count; ++q) *(volatile int32_t*)peers.fail[q] = f;
+    __threadfence_system();
+    for (int q = 0; q < peers.count; ++q) st_release_sys(peers.flags[q] + flag_idx, epoch);
+}
 
 template <int S>
 struct Pipe {
@@ -1234,14 +1273,16 @@ __global__ void __launch_bounds__(T, 1)
     k_casc_panel(double* __restrict__ cols, const double* __restrict__ a,
                  const double* __restrict__ d, double* __restrict__ denoms, int m, idx_t n,
                  idx_t q0, idx_t p0, idx_t p1, int32_t* __restrict__ fail, int* __restrict__ flags,
-                 int epoch, const int* __restrict__ uflag, int utag) {
+                 int epoch, const int* __restrict__ uflag, int utag, const PeerSet peers) {
     const idx_t tile = p0 / C + blockIdx.x;
     // a tile's final columns are published in NCH chunks of CH (flags[tile*NCH + ch])
     constexpr int CH = C / kPanelChunks > 0 ? C / kPanelChunks : 1;
     constexpr int NCH = C / CH;
     if (*(volatile int32_t*)fail) {  // still publish: later tiles may be waiting
-        if (threadIdx.x == 0)
+        if (threadIdx.x == 0) {
             for (int ch = 0; ch < NCH; ++ch) st_release(flags + tile * NCH + ch, epoch);
+            peer_signal(peers, fail, flags, tile * NCH + NCH - 1, epoch);
+        }
         return;
     }
     double *red, *bc;
@@ -1315,11 +1356,15 @@ __global__ void __launch_bounds__(T, 1)
             PANEL_LAP(t_apply);
         }
     }
+    bool stored = false;
     if (!dead) {
         const bool broken = panel_triangle<TMA, S, T, R, C, GEN>(
             tl, pp, a, denoms, m, col0, p1, q0, fail, bc, producer, cols, n,
             NCH > 1 ? flags + tile * NCH : nullptr, epoch);
-        if (!broken) tl.store(cols, col0, n + 1);
+        if (!broken) {
+            tl.store(cols, col0, n + 1);
+            stored = true;
+        }
 #if PDAS_PANEL_TRACE
         if (trace) {
             long long t_tri = 0;
@@ -1334,8 +1379,37 @@ __global__ void __launch_bounds__(T, 1)
     }
     __threadfence();
     __syncthreads();
+    if (peers.count > 0) {
+        // multi-GPU exchange fused into the panel: the tile's final columns go
+        // from registers straight into every peer's [Y|x] over NVLink, with
+        // their denominators; then one system-scope flag per peer and tile
+        if (stored) {
+            for (int q = 0; q < peers.count; ++q) tl.store(peers.cols[q], col0, n + 1);
+            if (threadIdx.x < C && col0 + threadIdx.x < p1) {
+                const double den = __ldcg(denoms + col0 + threadIdx.x);
+                for (int q = 0; q < peers.count; ++q) peers.denoms[q][col0 + threadIdx.x] = den;
+            }
+        }
+        __threadfence_system();
+        __syncthreads();
+        if (producer) peer_signal(peers, fail, flags, tile * NCH + NCH - 1, epoch);
+    }
     if (producer)
         for (int ch = 0; ch < NCH; ++ch) st_release(flags + tile * NCH + ch, epoch);
+}
+
+// Non-owner side of the fused exchange: wait until every tile of columns
+// [c0, c1) has been signalled by its owner's panel for this epoch.  Bounded:
+// a peer that never signals traps after 30 s instead of hanging the device.
+__global__ void k_peer_wait(const int* __restrict__ flags, idx_t t0, idx_t t1, int nch, int epoch) {
+    for (idx_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+        const int* f = flags + t * nch + nch - 1;
+        const unsigned long long start = global_ns();
+        while (ld_acquire_sys(f) != epoch) {
+            __nanosleep(64);
+            if (global_ns() - start > 30000000000ull) __trap();
+        }
+    }
 }
 
 // ------------------------------------------------------------ host side
@@ -1469,6 +1543,7 @@ struct CascOp {
     // cascade, when column n sits alone in the last tile (n % CT == 0).
     const double* x0_low = nullptr;
     double* x0_work = nullptr;
+    PeerSet peers{};  // kind 1 only: fused multi-GPU exchange
 };
 
 template <bool TMA, int S, int T, int R, int Cu, int G, int CT>
@@ -1502,7 +1577,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
     if (op.kind == 1) {
         if (op.p0 % CT || op.p1 <= op.p0 || op.p1 - op.q0 > 2 * kMaxBlock) return PDAS_ERR_ARG;
         kp<<<(unsigned)((op.p1 - op.p0 + CT - 1) / CT), T, smem_p, st>>>(
-            cols, a, d, denoms, m, n, op.q0, op.p0, op.p1, fail, flags, epoch, nullptr, 0);
+            cols, a, d, denoms, m, n, op.q0, op.p0, op.p1, fail, flags, epoch, nullptr, 0, op.peers);
         return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
     }
     if (op.kind == 2) {
@@ -1563,7 +1638,8 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         }
         prof.mark(ss.ps, 1, 0, 0);
         kp<<<(unsigned)tiles_of(0), T, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, 0, 0,
-                                                        blk_end(0), fail, flags, epoch, nullptr, 0);
+                                                        blk_end(0), fail, flags, epoch, nullptr, 0,
+                                                        PeerSet{});
         prof.mark(ss.ps, 1, 0, 1);
         cudaEventRecord(ss.eP, ss.ps);
         if (xlane) {
@@ -1596,7 +1672,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
                 prof.mark(ss.ps, 1, b + 1, 0);
                 kp<<<(unsigned)tiles_of(b + 1), T, smem_p, ss.ps>>>(
                     cols, a, d, denoms, m, n, p0, p0, blk_end(b + 1), fail, flags, epoch, uflag,
-                    (int)(b + 1));
+                    (int)(b + 1), PeerSet{});
                 prof.mark(ss.ps, 1, b + 1, 1);
                 cudaEventRecord(ss.eP, ss.ps);
                 if (xlane) {
@@ -1619,7 +1695,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
     cudaStreamWaitEvent(ss.ps, ss.e0, 0);
     cudaEventRecord(ss.eU, st);
     kp<<<(unsigned)tiles_of(0), T, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, 0, 0, blk_end(0),
-                                                    fail, flags, epoch, nullptr, 0);
+                                                    fail, flags, epoch, nullptr, 0, PeerSet{});
     cudaEventRecord(ss.eP, ss.ps);
     for (idx_t b = 0; b < nb; ++b) {
         cudaStreamWaitEvent(st, ss.eP, 0);  // panel(b): block b is final
@@ -1628,7 +1704,8 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
             cudaStreamWaitEvent(ss.ps, ss.eU, 0);
             kp<<<(unsigned)tiles_of(b + 1), T, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, b * B,
                                                                 (b + 1) * B, blk_end(b + 1), fail,
-                                                                flags, epoch, nullptr, 0);
+                                                                flags, epoch, nullptr, 0,
+                                                                PeerSet{});
             cudaEventRecord(ss.eP, ss.ps);
         }
         // U_rest(b): every tile beyond block b+1 (or beyond block b at the end)
@@ -1753,14 +1830,51 @@ int launch_cascade_x0(double* cols, const double* a, const double* d, const doub
 
 int launch_cascade_panel(double* cols, const double* a, const double* d, idx_t m, idx_t n,
                          idx_t q0, idx_t p0, idx_t p1, double* denoms, int32_t* fail_dev,
-                         int* flags, int epoch, cudaStream_t st) {
+                         int* flags, int epoch, cudaStream_t st, const PeerSet* peers) {
     if (m < 1 || m > INT_MAX / 4 || q0 < 0 || q0 > p0 || p1 > n) return PDAS_ERR_ARG;
     CascOp op;
     op.kind = 1;
     op.q0 = q0;
     op.p0 = p0;
     op.p1 = p1;
+    if (peers) {
+        if (peers->count < 0 || peers->count > kMaxPeers) return PDAS_ERR_ARG;
+        op.peers = *peers;
+    }
     return dispatch_cascade(cols, a, d, m, n, denoms, fail_dev, flags, epoch, kMaxBlock, st, op);
+}
+
+int launch_cascade_panel_peers(double* cols, const double* a, const double* d, idx_t m, idx_t n,
+                               idx_t q0, idx_t p0, idx_t p1, double* denoms, int32_t* fail_dev,
+                               int* flags, int epoch, int npeers, double* const* peer_cols,
+                               double* const* peer_denoms, int32_t* const* peer_fail,
+                               int* const* peer_flags, cudaStream_t st) {
+    if (npeers < 0 || npeers > kMaxPeers) return PDAS_ERR_ARG;
+    PeerSet ps{};
+    ps.count = npeers;
+    for (int q = 0; q < npeers; ++q) {
+        if (!peer_cols[q] || !peer_denoms[q] || !peer_fail[q] || !peer_flags[q]) return PDAS_ERR_ARG;
+        ps.cols[q] = peer_cols[q];
+        ps.denoms[q] = peer_denoms[q];
+        ps.fail[q] = peer_fail[q];
+        ps.flags[q] = peer_flags[q];
+    }
+    return launch_cascade_panel(cols, a, d, m, n, q0, p0, p1, denoms, fail_dev, flags, epoch, st,
+                                &ps);
+}
+
+int panel_flag_chunks(int ct) {
+    const int ch = ct / kPanelChunks > 0 ? ct / kPanelChunks : 1;
+    return ct / ch;
+}
+
+int launch_peer_wait(const int* flags, idx_t m, idx_t c0, idx_t c1, int epoch, cudaStream_t st) {
+    const int ct = cascade_cfg(m).CT;
+    if (ct < 1 || c0 < 0 || c1 < c0) return PDAS_ERR_ARG;
+    if (c1 == c0) return PDAS_OK;
+    const idx_t t0 = c0 / ct, t1 = (c1 + ct - 1) / ct;
+    k_peer_wait<<<1, 64, 0, st>>>(flags, t0, t1, panel_flag_chunks(ct), epoch);
+    return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
 }
 
 int launch_cascade_update(double* cols, const double* a, const double* d, idx_t m, idx_t n,

@@ -74,9 +74,17 @@ int launch_cascade(double* cols, const double* a, const double* d, idx_t m, idx_
 int launch_cascade_x0(double* cols, const double* a, const double* d, const double* low, idx_t m,
                       idx_t n, double* denoms, int32_t* fail_dev, int* flags, int epoch,
                       double* work, cudaStream_t st);
+constexpr int kMaxPeers = 7;  // one box: 8 GPUs
+struct PeerSet;              // cascade.cu
 int launch_cascade_panel(double* cols, const double* a, const double* d, idx_t m, idx_t n,
                          idx_t q0, idx_t p0, idx_t p1, double* denoms, int32_t* fail_dev,
-                         int* flags, int epoch, cudaStream_t st);
+                         int* flags, int epoch, cudaStream_t st, const PeerSet* peers = nullptr);
+int launch_cascade_panel_peers(double* cols, const double* a, const double* d, idx_t m, idx_t n,
+                               idx_t q0, idx_t p0, idx_t p1, double* denoms, int32_t* fail_dev,
+                               int* flags, int epoch, int npeers, double* const* peer_cols,
+                               double* const* peer_denoms, int32_t* const* peer_fail,
+                               int* const* peer_flags, cudaStream_t st);
+int launch_peer_wait(const int* flags, idx_t m, idx_t c0, idx_t c1, int epoch, cudaStream_t st);
 int launch_cascade_update(double* cols, const double* a, const double* d, idx_t m, idx_t n,
                           idx_t p0, idx_t p1, const int64_t* tiles, idx_t ntiles, double* denoms,
                           int32_t* fail_dev, cudaStream_t st);

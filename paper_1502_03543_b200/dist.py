@@ -40,6 +40,16 @@ performs it.  `run_collective` does it with torch.distributed (NCCL on GPUs,
 gloo in the CPU tests); `run_lockstep` drives G in-process virtual ranks in
 lock-step (the broadcast becomes a copy), which is how one GPU checks the
 sharded path without running ranks that wait on each other.
+
+Fused exchange (exchange="peer"): instead of broadcasting a
+block after its panel, the owner's panel kernel stores each finished tile
+from registers straight into every peer's [Y | x] (and denominators, fail
+word) through NVLink peer mappings and releases a per-tile flag there
+(pdas_cascade_panel_peers); a non-owner's side stream runs a wait kernel on
+those flags (pdas_cascade_peer_wait) where it would have joined the
+broadcast.  The peer addresses come from torch symmetric memory (one
+process per GPU) or, for the in-process virtual ranks, are the other ranks'
+buffers on the same device.
 """
 
 from __future__ import annotations
@@ -163,7 +173,9 @@ def run_collective(plan: ShardPlan, be, group=None) -> None:
 
     `be.block_views(c0, c1, p0, p1)` returns the tensors a block broadcast
     carries (columns, denominators, fail word); `be.x_view()` the x column.
-    Each broadcast is issued under the stream the schedule is on."""
+    Each broadcast is issued under the stream the schedule is on.  A backend
+    with `fused` set exchanges blocks itself (`be.exchange_block(op)`: the
+    owner's panel already stored them into the peers; others wait)."""
     import torch.distributed as dist
 
     ranks = None if group is None else dist.get_process_group_ranks(group)
@@ -171,8 +183,11 @@ def run_collective(plan: ShardPlan, be, group=None) -> None:
     def g(src):
         return src if ranks is None else ranks[src]
 
+    fused = getattr(be, "fused", False)
     for op in cascade_schedule(plan, be):
-        if op[0] == "block":
+        if op[0] == "block" and fused:
+            be.exchange_block(op)
+        elif op[0] == "block":
             _, b, src, c0, c1, p0, p1 = op
             for t in be.block_views(c0, c1, p0, p1):
                 dist.broadcast(t, g(src), group=group)
@@ -191,7 +206,10 @@ def run_lockstep(plans: Sequence[ShardPlan], bes: Sequence) -> None:
         if any(o != ops[0] for o in ops):
             raise RuntimeError(f"virtual ranks diverged: {ops}")
         op = ops[0]
-        if op[0] == "block":
+        if op[0] == "block" and all(getattr(be, "fused", False) for be in bes):
+            for be in bes:
+                be.exchange_block(op)
+        elif op[0] == "block":
             _, b, src, c0, c1, p0, p1 = op
             srcv = bes[src].block_views(c0, c1, p0, p1)
             for r, be in enumerate(bes):
@@ -214,7 +232,13 @@ class CudaShard(_NullBackend):
     streams=True: panels + block broadcasts on a high-priority side stream,
     updates on the caller's stream (the lookahead of the 1-GPU cascade)."""
 
-    def __init__(self, plan: ShardPlan, cols, a, d, ws, fail, streams: bool = True):
+    def __init__(self, plan: ShardPlan, cols, a, d, ws, fail, streams: bool = True,
+                 peers: Optional[Sequence[Tuple[int, int, int]]] = None):
+        """peers: for the fused exchange, (cols, ws, fail) device addresses of
+        every OTHER rank, in rank order, valid in this process; None = the
+        blocks travel by broadcast (run_collective) or copy (run_lockstep)."""
+        import ctypes
+
         from . import _device as dv
         from ._lib import call
 
@@ -227,6 +251,12 @@ class CudaShard(_NullBackend):
         self.tiles = t.from_numpy(plan.tiles.copy()).to(dv.device())
         self.epoch = 0
         self.streams = streams
+        self.fused = peers is not None
+        if self.fused:
+            if len(peers) != plan.world - 1:
+                raise ValueError("peers must list every other rank")
+            arr = ctypes.c_uint64 * max(len(peers), 1)
+            self._peer_arrays = tuple(arr(*[int(p[i]) for p in peers]) for i in range(3))
         if streams:
             lo, hi = t.cuda.Stream.priority_range()
             self.side_stream = t.cuda.Stream(priority=hi)
@@ -239,7 +269,8 @@ class CudaShard(_NullBackend):
     # -- stream hooks
     def begin(self) -> None:
         self.epoch += 1
-        self.fail.zero_()
+        if not self.fused:  # fused: the caller zeroes it before the peers may write it
+            self.fail.zero_()
         if self.streams:
             self.main = self.t.cuda.current_stream()
             self.side_stream.wait_stream(self.main)
@@ -263,8 +294,25 @@ class CudaShard(_NullBackend):
     # -- compute
     def panel(self, q0: int, p0: int, p1: int) -> None:
         p, dv = self.plan, self.dv
+        if self.fused:
+            pc, pw, pf = self._peer_arrays
+            self.call("pdas_cascade_panel_peers", dv.ptr(self.cols), dv.ptr(self.a),
+                      dv.ptr(self.d), p.m, p.n, q0, p0, p1, dv.ptr(self.ws), self.epoch,
+                      dv.ptr(self.fail), p.world - 1, pc, pw, pf, dv.stream())
+            return
         self.call("pdas_cascade_panel", dv.ptr(self.cols), dv.ptr(self.a), dv.ptr(self.d), p.m,
                   p.n, q0, p0, p1, dv.ptr(self.ws), self.epoch, dv.ptr(self.fail), dv.stream())
+
+    def exchange_block(self, op: Op) -> None:
+        """Fused exchange of a block: nothing to do on its owner (the panel
+        stored it into the peers); elsewhere the current stream waits for the
+        owner's per-tile flags."""
+        _, b, src, c0, c1, p0, p1 = op
+        if src == self.plan.rank:
+            return
+        p, dv = self.plan, self.dv
+        self.call("pdas_cascade_peer_wait", dv.ptr(self.ws), p.m, p.n, c0, c1, self.epoch,
+                  dv.stream())
 
     def update(self, p0: int, p1: int, i0: int) -> None:
         p, dv = self.plan, self.dv
@@ -311,24 +359,76 @@ class ShardedSolver(DeviceSolver):
     broadcasts plus one x-column broadcast per iteration."""
 
     def __init__(self, prob, group=None, rho: float = 0.9, basis=None, L0=None,
-                 block: Optional[int] = None):
+                 block: Optional[int] = None, exchange: str = "nccl"):
+        """exchange: "nccl" (a broadcast per block) or "peer" (the fused
+        exchange: [Y | x], the cascade workspace and the fail word live in
+        torch symmetric memory and the owner's panel stores into the peers)."""
         import torch.distributed as dist
 
         from ._lib import OFF_CASCADE_FAIL
 
+        if exchange not in ("nccl", "peer"):
+            raise ValueError(f"exchange must be 'nccl' or 'peer', not {exchange!r}")
         super().__init__(prob, "woodbury", rho, basis=basis, L0=L0)
         self.group = group
+        self.exchange = exchange
         world = dist.get_world_size(group)
         rank = dist.get_rank(group)
         self.plan = make_plan(self.m, self.n, world, rank, block)
-        fail = self.state[OFF_CASCADE_FAIL:OFF_CASCADE_FAIL + 4]
-        self.shard = CudaShard(self.plan, self.cols, prob.A, self.d, self.casc_ws, fail)
+        self._state_fail = self.state[OFF_CASCADE_FAIL:OFF_CASCADE_FAIL + 4]
+        peers = None
+        fail = self._state_fail
+        if exchange == "peer":
+            fail, peers = self._symmetric_buffers(world, rank)
+        self.shard = CudaShard(self.plan, self.cols, prob.A, self.d, self.casc_ws, fail,
+                               peers=peers)
         p = self.plan
         self._casc_launches = sum(1 for b in range(p.nb) if p.owns_block(b)) + sum(
             1 for b in range(p.nb) if p.update_start(b) < len(p.tiles))
 
+    def _symmetric_buffers(self, world: int, rank: int):
+        """Move [Y | x], the cascade workspace and a fail word into one
+        symmetric-memory allocation; return (fail view, peer addresses)."""
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+
+        t, m, n = self.t, self.m, self.n
+        from . import _device as dv
+
+        def up(x):
+            return (x + 255) // 256 * 256
+
+        ncol = m * (n + 1) * 8
+        wsb = self.casc_ws.numel()
+        off_ws = up(ncol)
+        off_fail = up(off_ws + wsb)
+        buf = symm.empty(off_fail + 256, dtype=t.uint8, device=dv.device())
+        buf.zero_()
+        g = self.group if self.group is not None else dist.group.WORLD
+        handle = symm.rendezvous(buf, g.group_name)
+        ptrs = [int(p) for p in handle.buffer_ptrs]
+        self._symm = (buf, handle)
+        self.cols = buf[:ncol].view(t.float64)
+        self.xcol = self.cols[m * n:]
+        self.casc_ws = buf[off_ws:off_ws + wsb]
+        fail = buf[off_fail:off_fail + 4].view(t.int32)
+        self._sync = t.zeros(1, dtype=t.int32, device=dv.device())
+        peers = [(ptrs[r], ptrs[r] + off_ws, ptrs[r] + off_fail) for r in range(world)
+                 if r != rank]
+        return fail, peers
+
     def _cascade(self) -> None:
-        run_collective(self.plan, self.shard, self.group)
+        if self.exchange == "peer":
+            import torch.distributed as dist
+
+            # every rank has re-seeded [Y | x] and finished the previous
+            # cascade before any peer's panel may store into it
+            self.shard.fail.zero_()
+            dist.all_reduce(self._sync, group=self.group)
+            run_collective(self.plan, self.shard, self.group)
+            self._state_fail.copy_(self.shard.fail.view(self.t.uint8))
+        else:
+            run_collective(self.plan, self.shard, self.group)
         self.launches += self._casc_launches
 
     def _cascade_x0(self) -> None:
@@ -340,11 +440,17 @@ class ShardedSolver(DeviceSolver):
 
 
 def solve_sweeps_virtual(cols: np.ndarray, a: np.ndarray, d: np.ndarray, world: int,
-                         block: Optional[int] = None) -> Tuple[int, List[np.ndarray]]:
+                         block: Optional[int] = None, fused: bool = False,
+                         reps: int = 1) -> Tuple[int, List[np.ndarray]]:
     """The sharded cascade over `world` virtual ranks on the current GPU, in
     lock-step (no rank waits on another inside a kernel).  Returns the common
     fail code and every rank's final [Y | x] (host copies, column-major).
-    Verification entry point for the multi-GPU schedule."""
+    fused: blocks move by the panel's peer stores + flag waits (the other
+    virtual ranks' buffers stand in for the NVLink peer mappings); by the
+    time a rank's wait kernel runs, the owner's panel has been enqueued
+    before it on the same stream.  reps > 1 re-runs the cascade from the same
+    input (new epoch each time: stale flags of the previous run must not
+    satisfy a wait).  Verification entry point for the multi-GPU schedule."""
     from . import _device as dv
     from ._lib import load
 
@@ -353,15 +459,23 @@ def solve_sweeps_virtual(cols: np.ndarray, a: np.ndarray, d: np.ndarray, world: 
     A = dv.upload(np.asfortranarray(a))
     dd = dv.upload(np.ascontiguousarray(d, dtype=np.float64))
     wsb = int(load().pdas_cascade_ws_bytes(m, n))
-    plans, bes = [], []
+    plans, bufs, bes = [], [], []
+    c_in = dv.upload(np.asfortranarray(cols))
     for r in range(world):
-        plan = make_plan(m, n, world, r, block)
-        c = dv.upload(np.asfortranarray(cols))
-        ws = t.zeros(wsb, dtype=t.uint8, device=dv.device())
-        fail = t.zeros(1, dtype=t.int32, device=dv.device())
-        plans.append(plan)
-        bes.append(CudaShard(plan, c, A, dd, ws, fail, streams=False))
-    run_lockstep(plans, bes)
+        plans.append(make_plan(m, n, world, r, block))
+        bufs.append((c_in.clone(), t.zeros(wsb, dtype=t.uint8, device=dv.device()),
+                     t.zeros(1, dtype=t.int32, device=dv.device())))
+    for r in range(world):
+        peers = None
+        if fused:
+            peers = [tuple(dv.ptr(x) for x in bufs[q]) for q in range(world) if q != r]
+        c, ws, fail = bufs[r]
+        bes.append(CudaShard(plans[r], c, A, dd, ws, fail, streams=False, peers=peers))
+    for rep in range(reps):
+        for (c, _, fail) in bufs:
+            c.copy_(c_in)
+            fail.zero_()
+        run_lockstep(plans, bes)
     dv.synchronize()
     fails = [int(be.fail.item()) for be in bes]
     if len(set(fails)) != 1:

@@ -262,6 +262,7 @@ def solve_lp(
     opts: Optional[SolveOptions] = None,
     *,
     group=None,
+    exchange: str = "nccl",
 ) -> Tuple[InteriorPoint, Status, List[TraceRecord]]:
     """Run the affine-scaling iteration from a strictly feasible start.
 
@@ -272,7 +273,9 @@ def solve_lp(
     group: a torch.distributed process group (one process per GPU, every rank
     calling with the same problem): the Woodbury cascade then runs
     column-sharded over the group (dist.py); results are bitwise the 1-GPU
-    ones on every rank.
+    ones on every rank.  exchange: "nccl" (one broadcast per pivot block) or
+    "peer" (the panel stores finished blocks straight into the peers' buffers
+    over NVLink, torch symmetric memory; dist.ShardedSolver).
     """
     opts = opts or SolveOptions()
     prob = DeviceProblem.from_lp(lp)
@@ -284,7 +287,7 @@ def solve_lp(
     if group is not None and opts.backend == "woodbury":
         from .dist import ShardedSolver
 
-        eng = ShardedSolver(prob, group, opts.rho, L0=L0)
+        eng = ShardedSolver(prob, group, opts.rho, L0=L0, exchange=exchange)
     else:
         eng = DeviceSolver(prob, opts.backend, opts.rho,
                            L0=L0 if opts.backend == "woodbury" else None)

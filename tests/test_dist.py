@@ -201,3 +201,60 @@ def test_gloo_processes_bitwise(world):
     cases = [(7, 45, 4, 2, 1, None), (8, 40, 8, 4, 2, None), (5, 33, 8, 8, 3, None),
              (6, 41, 4, 2, 7, 22)]
     mp.spawn(_worker, args=(world, _free_port(), cases), nprocs=world, join=True)
+
+
+class FusedOracleShard(OracleShard):
+    """The fused exchange's contract on CPU: the owner's panel itself stores
+    the block's final columns, denominators and fail word into every peer and
+    raises a per-(epoch, tile) flag there; a non-owner's exchange_block only
+    checks that its flags are up (the GPU wait kernel)."""
+
+    fused = True
+
+    def __init__(self, plan, cols, a, d):
+        super().__init__(plan, cols, a, d)
+        self.peers = []
+        self.flags = set()
+        self.epoch = 0
+
+    def begin(self):
+        self.epoch += 1
+
+    def panel(self, q0, p0, p1):
+        super().panel(q0, p0, p1)
+        c0, c1 = self.plan.block_columns(p0 // self.plan.B)
+        m, w = self.plan.m, self.plan.w
+        for peer in self.peers:
+            if not self.fail[0]:
+                peer.flat[c0 * m:c1 * m] = self.flat[c0 * m:c1 * m]
+                peer.denoms[p0:p1] = self.denoms[p0:p1]
+            else:
+                peer.fail[0] = self.fail[0]
+            peer.flags.update((self.epoch, t) for t in range(c0 // w, (c1 + w - 1) // w))
+
+    def exchange_block(self, op):
+        _, b, src, c0, c1, p0, p1 = op
+        if src != self.plan.rank:
+            w = self.plan.w
+            missing = [t for t in range(c0 // w, (c1 + w - 1) // w) if (self.epoch, t) not in self.flags]
+            assert not missing, (self.plan.rank, b, missing)
+
+
+@pytest.mark.parametrize("m,n,world,B,w,step", [
+    (7, 45, 2, 4, 2, None), (9, 41, 3, 8, 4, None), (6, 64, 4, 16, 8, None),
+    (12, 63, 5, 8, 8, None), (6, 41, 3, 4, 2, 22), (6, 41, 3, 4, 2, 0),
+])
+def test_lockstep_fused_exchange(m, n, world, B, w, step):
+    a, d, cols = _system(m, n, 13 * m + n, skip=0.0 if step is not None else 0.15)
+    if step is not None:
+        d = _breakdown_d(a, d, cols, step)
+    ret, ref = _serial(a, d, cols)
+    plans = [D.ShardPlan(m, n, world, r, B, w) for r in range(world)]
+    bes = [FusedOracleShard(p, cols, a, d) for p in plans]
+    for be in bes:
+        be.peers = [q for q in bes if q is not be]
+    D.run_lockstep(plans, bes)
+    assert [int(be.fail[0]) for be in bes] == [ret] * world
+    if ret == 0:
+        for be in bes:
+            assert bits_equal(be.cols, ref)

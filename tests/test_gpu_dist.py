@@ -6,7 +6,13 @@ runs as G virtual ranks in lock-step (each with its own [Y | x], workspace
 and fail word; a broadcast is a device copy).  Every rank's result must be
 bitwise the serial oracle cascade (_kernels.pyx:234-291).  The real
 collective driver (NCCL, side-stream lookahead) is exercised with a
-one-rank NCCL group through solve_lp(group=...)."""
+one-rank NCCL group through solve_lp(group=...).
+
+The fused exchange (pdas_cascade_panel_peers / pdas_cascade_peer_wait: the
+owner's panel stores its tiles into the peers' buffers and flags them) runs
+the same way: the virtual ranks' buffers stand in for NVLink peer mappings,
+and each wait kernel is enqueued after the owner's panel, so no kernel ever
+waits on one that has not been launched."""
 
 import socket
 
@@ -55,6 +61,39 @@ def test_virtual_ranks_bitwise(gpu, m, n, world, block):
     assert fail == 0
     for r, c in enumerate(outs):
         assert bits_equal(c, ref), r
+
+
+@pytest.mark.parametrize("m,n,world,block", [
+    (40, 300, 2, None), (64, 129, 3, 16), (300, 520, 8, 32), (500, 1000, 4, None),
+    (1000, 1024, 5, 16), (2000, 2100, 3, None), (2000, 2048, 8, 8), (3000, 300, 2, 4),
+])
+def test_virtual_ranks_fused_exchange_bitwise(gpu, m, n, world, block):
+    from paper_1502_03543_b200 import dist as D
+
+    a, d, cols = _system(m, n, 5 * m + n + world)
+    ret, ref = _serial(a, d, cols)
+    assert ret == 0
+    # two runs: the second must not be satisfied by the first run's flags
+    fail, outs = D.solve_sweeps_virtual(cols, a, d, world, block, fused=True, reps=2)
+    assert fail == 0
+    for r, c in enumerate(outs):
+        assert bits_equal(c, ref), r
+
+
+@pytest.mark.parametrize("step", [3, 130, 517])
+def test_virtual_ranks_fused_breakdown(gpu, step):
+    """A breakdown in a block owned by one rank reaches the others through the
+    panel's peer fail-word store; every rank returns the same 1-based step."""
+    from paper_1502_03543_b200 import dist as D
+
+    m, n = 100, 600
+    a, d, cols = _system(m, n, 11, skip=0.0)
+    R = O.restated()
+    c = cols.copy(order="F")
+    assert R.solve_sweeps_prefix(c, a, d, np.zeros(n + 1), np.zeros(m), step, 1) == 0
+    d[step] = 1.0 - 1.0 / R.dot_tree(a[:, step], c[:, step])
+    fail, _ = D.solve_sweeps_virtual(cols, a, d, 3, 16, fused=True)
+    assert fail == step + 1
 
 
 @pytest.mark.parametrize("step", [3, 130, 517])
@@ -114,6 +153,28 @@ def test_sharded_solver_c2_first_iterations(gpu, nccl_group):
     lp, start = P.gen_random_feasible(500, 5000, 0)
     outs = []
     for mk in (lambda pr: DeviceSolver(pr), lambda pr: D.ShardedSolver(pr, nccl_group)):
+        prob = DeviceProblem.from_lp(lp)
+        eng = mk(prob)
+        eng.load_iterate(start.x, start.y, start.s)
+        sts = [eng.iterate().state for _ in range(2)]
+        outs.append(([(s.alpha, s.gap, s.blocking) for s in sts], eng.read_iterate()))
+    assert outs[0][0] == outs[1][0]
+    for u, v in zip(outs[0][1], outs[1][1]):
+        assert bits_equal(u, v)
+
+
+def test_sharded_solver_peer_exchange(gpu, nccl_group):
+    """exchange="peer": [Y | x], workspace and fail word in torch symmetric
+    memory (rendezvous over the group), the per-iteration barrier, fused
+    panel entry point; two c2 iterations bitwise against the 1-GPU engine."""
+    P = gpu
+    from paper_1502_03543_b200 import dist as D
+    from paper_1502_03543_b200.engine import DeviceProblem, DeviceSolver
+
+    lp, start = P.gen_random_feasible(500, 5000, 0)
+    outs = []
+    for mk in (lambda pr: DeviceSolver(pr),
+               lambda pr: D.ShardedSolver(pr, nccl_group, exchange="peer")):
         prob = DeviceProblem.from_lp(lp)
         eng = mk(prob)
         eng.load_iterate(start.x, start.y, start.s)
