@@ -37,6 +37,9 @@
 #include "pdas_internal.h"
 #include "tma.cuh"
 
+#ifndef PDAS_WS_PTRS
+#define PDAS_WS_PTRS 1
+#endif
 #ifndef PDAS_PANEL_TMA
 #define PDAS_PANEL_TMA 1
 #endif
@@ -851,6 +854,21 @@ __device__ __forceinline__ void ws_compute_ldg(Tile<TC, R, C, false>& tl,
             vh[r] = (FULL || tl.vhi(r)) ? nah[r] * f : 0.0;
         }
     };
+#if PDAS_WS_PTRS
+    // loop-carried per-thread column pointers (this thread's first row folded
+    // in): the loads need no per-pivot address rebuild (S2R/LDC chains the
+    // compiler otherwise rematerialises under register pressure)
+    const int H = tl.H;
+    auto ldp = [&](const double* p, double (&lo)[R], double (&hi)[R]) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            lo[r] = __ldcg(p + TC * r);
+            hi[r] = (FULL || tl.vhi(r)) ? __ldcg(p + H + TC * r) : 0.0;
+        }
+    };
+    const double* pnext = pcol + m + tl.t;
+    const double* anext = acol + 2 * (size_t)m + tl.t;
+#endif
     // prologue: v_0, P_0 and A_1 in registers / in flight
     tl.template load_p<true, FULL>(acol, nal, nah);
     tl.template load_p<true, FULL>(pcol, npl, nph);
@@ -886,10 +904,20 @@ __device__ __forceinline__ void ws_compute_ldg(Tile<TC, R, C, false>& tl,
             pl[r] = npl[r];
             ph[r] = nph[r];
         }
+#if PDAS_WS_PTRS
+        if (j + 1 < cnt) ldp(pnext, npl, nph);
+        pnext += m;
+#else
         if (j + 1 < cnt) tl.template load_p<true, FULL>(pcol + (size_t)(j + 1) * m, npl, nph);
+#endif
         if (a_cur) axpy(0, bcA);
         scale(dn - 1.0);
+#if PDAS_WS_PTRS
+        if (j + 2 < cnt) ldp(anext, nal, nah);
+        anext += m;
+#else
         if (j + 2 < cnt) tl.template load_p<true, FULL>(acol + (size_t)(j + 2) * m, nal, nah);
+#endif
         if (a_next) partials(0, redA);
         named_arrive(1, NT);
         WS_MARK(0, j, 4);
