@@ -37,6 +37,9 @@
 #include "pdas_internal.h"
 #include "tma.cuh"
 
+#ifndef PDAS_WS_SADDR
+#define PDAS_WS_SADDR 1
+#endif
 #ifndef PDAS_WS_PTRS
 #define PDAS_WS_PTRS 1
 #endif
@@ -91,6 +94,20 @@ __device__ __forceinline__ int ld_acquire_sys(const int* p) {
     int v;
     asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+
+// a value the compiler must keep in a register (it cannot rematerialise it)
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
+    asm volatile("" : "+r"(v));
+    return v;
+}
+
+__device__ __forceinline__ void st_shared_f64(uint32_t a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v));
+}
+
+__device__ __forceinline__ void ld_shared_v2_f64(uint32_t a, double& x, double& y) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
 }
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -813,6 +830,14 @@ __device__ __forceinline__ void ws_compute_ldg(Tile<TC, R, C, false>& tl,
     constexpr int HC = C / 2, NT = TC + 128;
     double vl[R], vh[R], pl[R], ph[R];
     double npl[R], nph[R], nal[R], nah[R];  // P_{j+1}, raw A_{j+2} in flight
+#if PDAS_WS_SADDR
+    // 32-bit shared addresses computed once and made opaque, so the loop
+    // does not rebuild the shared window base (S2UR/ULEA) and the thread
+    // index (S2R) for every reduction store and multiplier load
+    const uint32_t sa_red[2] = {opaque_u32(smem_addr(redA + tl.t)),
+                                opaque_u32(smem_addr(redB + tl.t))};
+    const uint32_t sa_bc[2] = {opaque_u32(smem_addr(bcA)), opaque_u32(smem_addr(bcB))};
+#endif
     auto partials = [&](int h0, double* red) {
 #pragma unroll
         for (int c = 0; c < HC; ++c) {
@@ -823,13 +848,28 @@ __device__ __forceinline__ void ws_compute_ldg(Tile<TC, R, C, false>& tl,
                 double hi = vh[r] * tl.xh[r][h0 + c];
                 s[r] = lo + hi;
             }
+#if PDAS_WS_SADDR
+            st_shared_f64(sa_red[h0 ? 1 : 0] + 8u * (uint32_t)(c * TC), lane_tree<R>(s));
+#else
             red[c * TC + tl.t] = lane_tree<R>(s);
+#endif
         }
     };
     auto axpy = [&](int h0, const double* bc) {
         double g[HC];
+#if PDAS_WS_SADDR
+        if constexpr (HC % 2 == 0) {
+#pragma unroll
+            for (int c = 0; c < HC; c += 2)
+                ld_shared_v2_f64(sa_bc[h0 ? 1 : 0] + 8u * c, g[c], g[c + 1]);
+        } else {
+#pragma unroll
+            for (int c = 0; c < HC; ++c) g[c] = bc[c];
+        }
+#else
 #pragma unroll
         for (int c = 0; c < HC; ++c) g[c] = bc[c];
+#endif
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const bool hi = FULL || tl.vhi(r);
