@@ -106,6 +106,12 @@ __device__ __forceinline__ void st_shared_f64(uint32_t a, double v) {
     asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v));
 }
 
+__device__ __forceinline__ double ld_shared_f64(uint32_t a) {
+    double x;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(a));
+    return x;
+}
+
 __device__ __forceinline__ void ld_shared_v2_f64(uint32_t a, double& x, double& y) {
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
 }
@@ -999,6 +1005,45 @@ __device__ __forceinline__ void ws_reducer_ldg(const double* sd, const double* s
             }
         }
     };
+#if PDAS_WS_SADDR
+    if constexpr (HC <= 4 && !PDAS_HOIST_WS && !PDAS_WS_TRACE) {
+        // one column per warp: its reduction rows, its multiplier slot and the
+        // pivot scalars as pinned 32-bit shared addresses (no per-pivot
+        // shared-window rebuild, as in ws_compute_ldg)
+        const bool mine = w < HC;
+        const uint32_t ra[2] = {opaque_u32(smem_addr(redA + w * TC + lane)),
+                                opaque_u32(smem_addr(redB + w * TC + lane))};
+        const uint32_t ba[2] = {opaque_u32(smem_addr(bcA + w)), opaque_u32(smem_addr(bcB + w))};
+        const uint32_t sda = opaque_u32(smem_addr(sd)), sna = opaque_u32(smem_addr(sden));
+        auto reduce1 = [&](int h, double denom) {
+            if (mine) {
+                double q[NW];
+#pragma unroll
+                for (int i = 0; i < NW; ++i) q[i] = ld_shared_f64(ra[h] + 256u * i);
+                const double u = warp_butterfly32(lane_tree<NW>(q));
+                const double g = u / denom;
+                if (lane == 0) st_shared_f64(ba[h], g);
+            }
+        };
+        bool act = ld_shared_f64(sda) != 1.0;
+        double den = ld_shared_f64(sna);
+        for (int j = 0; j < cnt; ++j) {
+            const uint32_t jn = (uint32_t)(j + 1 < cnt ? j + 1 : j);
+            const bool act_n = ld_shared_f64(sda + 8u * jn) != 1.0;
+            const double den_n = ld_shared_f64(sna + 8u * jn);
+            named_bar(1, NT);  // partials A(j) published
+            if (act) reduce1(0, den);
+            named_arrive(3, NT);
+            named_bar(2, NT);  // partials B(j) published
+            if (act) reduce1(1, den);
+            named_arrive(4, NT);
+            act = act_n;
+            den = den_n;
+        }
+        named_bar(1, NT);  // the compute warps' final PA arrival
+        return;
+    }
+#endif
     bool act = sd[0] != 1.0;
     double den = sden[0], y = sy[0];
     for (int j = 0; j < cnt; ++j) {
