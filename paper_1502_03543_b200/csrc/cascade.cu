@@ -696,11 +696,13 @@ __device__ __forceinline__ void apply_global(Tile<T, R, C, GEN>& tl, Pipe<S>& pp
 #endif
 constexpr int kWsT = 256;       // compute threads
 constexpr int kWsThreads = 384; // + reducer warpgroup
+// compute 224 / reducer 56 (c3 -0.9% vs 232 / 40: the reducer keeps its pivot scalars and
+// addresses in registers; the compute tile still fits without spills)
 #ifndef PDAS_WS_REGS_R
-#define PDAS_WS_REGS_R 40
+#define PDAS_WS_REGS_R 56
 #endif
 #ifndef PDAS_WS_REGS_C
-#define PDAS_WS_REGS_C 232
+#define PDAS_WS_REGS_C 224
 #endif
 constexpr int kWsRegsCompute = PDAS_WS_REGS_C, kWsRegsReducer = PDAS_WS_REGS_R;
 
