@@ -196,6 +196,13 @@ int pdas_iter_directions(const double* a, int64_t m, int64_t n, const double* dy
                          const double* d, const double* x, const double* s, double* dx,
                          double* ds, double rho, PdasIterState* state, void* stream);
 
+/* The damped ratio test alone on given directions (the public step_length,
+ * solver.py:175-189): state->alpha = rho * min(-x/dx | dx < 0, -s/ds | ds < 0),
+ * CAP_ALPHA (1e6) when no component blocks; state->blocking = first argmin over
+ * [x ratios | s ratios] (-1 if none).  state is reset by the caller. */
+int pdas_ratio_test(const double* x, const double* s, const double* dx, const double* ds,
+                    int64_t n, double rho, PdasIterState* state, void* stream);
+
 /* x += alpha*dx, y += alpha*dy, s += alpha*ds when state->stepped (solver.py:257-259). */
 int pdas_iter_update(double* x, double* y, double* s, const double* dx, const double* dy,
                      const double* ds, int64_t n, int64_t m, const PdasIterState* state,

@@ -19,6 +19,14 @@ mkdir -p "$out"
 py="${PYTHON:-python3}"
 ext="$($py -c 'import sysconfig; print(sysconfig.get_config_var("EXT_SUFFIX"))')"
 so="$out/_kernels$ext"
+# the reference's UNMODIFIED Python package, staged next to its compiled core
+# (git-ignored; travels to the GPU box) for the plugin-boundary test
+# (tests/test_gpu_plugin.py: the reference's own solve_lp over the B200 table)
+pkg="$(dirname "$src")"
+mkdir -p "$out/pkg/adascale"
+for f in "$pkg"/*.py; do
+  [ "$out/pkg/adascale/$(basename "$f")" -nt "$f" ] || cp "$f" "$out/pkg/adascale/"
+done
 if [ -f "$so" ] && [ "$so" -nt "$src" ]; then
   exit 0
 fi

@@ -88,6 +88,7 @@ SIGNATURES = {
     "pdas_iter_reset": (ctypes.c_int, [_VP, _VP]),
     "pdas_iter_scaling": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
     "pdas_iter_directions": (ctypes.c_int, [_VP, _I64, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _D, _VP, _VP]),
+    "pdas_ratio_test": (ctypes.c_int, [_VP, _VP, _VP, _VP, _I64, _D, _VP, _VP]),
     "pdas_iter_update": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _VP, _VP]),
     "pdas_iter_objectives": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _I64, _I64, _VP, _VP]),
     "pdas_probe_fp64": (ctypes.c_int, [_VP, _I64, _VP, _VP]),

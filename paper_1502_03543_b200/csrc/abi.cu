@@ -366,6 +366,17 @@ int pdas_iter_directions(const double* a, int64_t m, int64_t n, const double* dy
     return check_cuda(rc, "iter_directions");
 }
 
+int pdas_ratio_test(const double* x, const double* s, const double* dx, const double* ds,
+                    int64_t n, double rho, PdasIterState* state, void* stream) {
+    if (n < 1) return set_err(PDAS_ERR_ARG, "ratio_test: bad shape");
+    cudaStream_t st = S(stream);
+    void* parts = nullptr;
+    int rc = scratch((unsigned char**)&parts, (size_t)pdas::ratio_partials_bytes(n), st);
+    if (!rc) rc = pdas::launch_ratio_test(x, s, dx, ds, n, rho, parts, state, st);
+    if (parts) cudaFreeAsync(parts, st);
+    return check_cuda(rc, "ratio_test");
+}
+
 int pdas_iter_update(double* x, double* y, double* s, const double* dx, const double* dy,
                      const double* ds, int64_t n, int64_t m, const PdasIterState* state,
                      void* stream) {

@@ -1178,7 +1178,6 @@ __global__ void __launch_bounds__(TC + 128, TC == 128 ? 2 : 1)
     constexpr bool kLdg = PDAS_WS_LDG && R <= 4;
     constexpr int kRegC = TC == 256 ? kWsRegsCompute : (kLdg ? 208 : 216);
     constexpr int kRegR = TC == 256 ? kWsRegsReducer : (kLdg ? 48 : 40);
-    if (*(volatile const int32_t*)fail) return;
     double *red, *bc;
     Pipe<S> pp;
     carve<TC, C, 1, S>(red, bc, pp, false, m);
@@ -1187,7 +1186,9 @@ __global__ void __launch_bounds__(TC + 128, TC == 128 ? 2 : 1)
         mbar_fence_init();
     }
     stage_scalars(pp, d, denoms, p0, p0, p1, true);
-    __syncthreads();
+    // a breakdown found by a concurrent panel: one thread reads the fail word and
+    // the whole CTA leaves together (before setmaxnreg and the barrier protocol)
+    if (__syncthreads_or(threadIdx.x == 0 && *(volatile const int32_t*)fail != 0)) return;
     const int cnt = (int)(p1 - p0);
     constexpr int HC = C / 2;
     double* redA = red;
@@ -1239,12 +1240,11 @@ __global__ void __launch_bounds__(T* G, 1)
                   idx_t p0, idx_t p1, idx_t tile0, const int32_t* __restrict__ fail,
                   const int64_t* __restrict__ tiles, int* __restrict__ uflag, int utag,
                      int ucount) {
-    if (*(volatile const int32_t*)fail) return;
     double *red, *bc;
     Pipe<S> pp;
     carve<T, C, G, S>(red, bc, pp, TMA, m);
     stage_scalars(pp, d, denoms, p0, p0, p1, true);
-    __syncthreads();
+    if (__syncthreads_or(threadIdx.x == 0 && *(volatile const int32_t*)fail != 0)) return;
     const int grp = threadIdx.x / T;
     Tile<T, R, C, GEN> tl;
     tl.init(threadIdx.x % T, m, 1 + grp, red + grp * C * T, bc + grp * C);
@@ -1393,7 +1393,9 @@ __global__ void __launch_bounds__(T, 1)
     // a tile's final columns are published in NCH chunks of CH (flags[tile*NCH + ch])
     constexpr int CH = C / kPanelChunks > 0 ? C / kPanelChunks : 1;
     constexpr int NCH = C / CH;
-    if (*(volatile int32_t*)fail) {  // still publish: later tiles may be waiting
+    // block-uniform: thread 0 reads the fail word for the whole CTA
+    if (__syncthreads_or(threadIdx.x == 0 && *(volatile int32_t*)fail != 0)) {
+        // still publish: later tiles may be waiting
         if (threadIdx.x == 0) {
             for (int ch = 0; ch < NCH; ++ch) st_release(flags + tile * NCH + ch, epoch);
             peer_signal(peers, fail, flags, tile * NCH + NCH - 1, epoch);
@@ -1420,8 +1422,7 @@ __global__ void __launch_bounds__(T, 1)
                 if (*(volatile int32_t*)fail) break;
                 __nanosleep(64);
             }
-        __syncthreads();
-        dead = *(volatile int32_t*)fail != 0;
+        dead = __syncthreads_or(producer && *(volatile int32_t*)fail != 0);
     }
     if (!dead) {
         tl.load(cols, col0, n + 1);
@@ -1450,9 +1451,11 @@ __global__ void __launch_bounds__(T, 1)
         for (int ch = prev ? 0 : NCH - 1; ch < NCH; ++ch) {
             if (producer)
                 while (ld_acquire(flags + tp * NCH + ch) != epoch) __nanosleep(32);
-            __syncthreads();
+            // the flag's acquire and the fail word are read by one thread; the
+            // barrier hands both to the CTA (block-uniform exit)
+            const int broken = __syncthreads_or(producer && *(volatile int32_t*)fail != 0);
             PANEL_LAP(t_wait);
-            if (*(volatile int32_t*)fail) {
+            if (broken) {
                 dead = true;
                 break;
             }

@@ -41,6 +41,9 @@ int launch_directions(const double* a, idx_t m, idx_t n, const double* dy, const
                       const double* x, const double* s, double* dx, double* ds, void* partials,
                       cudaStream_t st);
 idx_t directions_partials_bytes(idx_t n);
+idx_t ratio_partials_bytes(idx_t n);
+int launch_ratio_test(const double* x, const double* s, const double* dx, const double* ds,
+                      idx_t n, double rho, void* partials, IterState* state, cudaStream_t st);
 int launch_dir_finish(const void* partials, idx_t n, const double* adx, idx_t m, const double* dy,
                       double rho, IterState* state, cudaStream_t st);
 int launch_update(double* x, double* y, double* s, const double* dx, const double* dy,

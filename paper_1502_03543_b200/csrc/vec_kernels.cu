@@ -430,6 +430,49 @@ __global__ void k_update(double* __restrict__ x, double* __restrict__ y, double*
     }
 }
 
+// The ratio test alone on given directions (the public step_length,
+// solver.py:175-189): per-block partial of min(-x/dx | dx<0) and
+// min(-s/ds | ds<0) with the first-occurrence index; k_dir_finish folds them.
+__global__ void __launch_bounds__(256) k_ratio_part(const double* __restrict__ x,
+                                                    const double* __restrict__ s,
+                                                    const double* __restrict__ dx,
+                                                    const double* __restrict__ ds, idx_t n,
+                                                    DirPartial* __restrict__ partials) {
+    __shared__ DirPartial sp[8];
+    DirPartial p;
+    p.max_rdual = 0.0;
+    p.max_rcomp = 0.0;
+    p.min_ratio = __longlong_as_double(0x7ff0000000000000LL);
+    p.argmin = -1;
+    p.nonfinite = 0;
+    p.pad = 0;
+    auto take = [&](double r, long long idx) {
+        if (p.argmin < 0 || r < p.min_ratio || (r == p.min_ratio && idx < p.argmin)) {
+            p.min_ratio = r;
+            p.argmin = idx;
+        }
+    };
+    for (idx_t j = (idx_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+         j += (idx_t)gridDim.x * blockDim.x) {
+        const double dxj = dx[j], dsj = ds[j];
+        if (dxj < 0.0) take(-x[j] / dxj, j);
+        if (dsj < 0.0) take(-s[j] / dsj, n + j);
+    }
+    for (int k = 16; k >= 1; k >>= 1) {
+        const double r = __shfl_xor_sync(0xffffffffu, p.min_ratio, k);
+        const long long i = __shfl_xor_sync(0xffffffffu, p.argmin, k);
+        if (i >= 0) take(r, i);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) sp[warp] = p;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w)
+            if (sp[w].argmin >= 0) take(sp[w].min_ratio, sp[w].argmin);
+        partials[blockIdx.x] = p;
+    }
+}
+
 // ----------------------------------------------------------- host launchers
 int launch_scaling(const double* x, const double* s, idx_t n, double* d, unsigned* flags,
                    cudaStream_t st) {
@@ -460,6 +503,22 @@ int launch_dir_finish(const void* partials, idx_t n, const double* adx, idx_t m,
     k_dir_finish<<<1, 1024, 0, st>>>((const DirPartial*)partials, np_, adx, m, dy, rho, state);
     return PDAS_OK;
 }
+
+idx_t ratio_partials_count(idx_t n) {
+    const idx_t g = (n + 255) / 256;
+    return g < 1184 ? (g > 0 ? g : 1) : 1184;
+}
+
+int launch_ratio_test(const double* x, const double* s, const double* dx, const double* ds,
+                      idx_t n, double rho, void* partials, IterState* state, cudaStream_t st) {
+    const idx_t g = ratio_partials_count(n);
+    k_ratio_part<<<(unsigned)g, 256, 0, st>>>(x, s, dx, ds, n, (DirPartial*)partials);
+    k_dir_finish<<<1, 1024, 0, st>>>((const DirPartial*)partials, (int)g, nullptr, 0, nullptr, rho,
+                                     state);
+    return PDAS_OK;
+}
+
+idx_t ratio_partials_bytes(idx_t n) { return ratio_partials_count(n) * (idx_t)sizeof(DirPartial); }
 
 int launch_update(double* x, double* y, double* s, const double* dx, const double* dy,
                   const double* ds, idx_t n, idx_t m, const IterState* state, cudaStream_t st) {

@@ -173,11 +173,32 @@ def make_backend(lp: StandardFormLP, name: str, workers: int = 1):
 
 
 # ------------------------------------------------------------------ pieces
-def scaling_diag(p: InteriorPoint) -> np.ndarray:
-    """d = x/s, the only iteration-dependent part of the normal equations."""
-    check_interior(p)
+def _state_scratch():
     t = dv.require_gpu()
-    return dv.download(t.div(dv.upload(p.x), dv.upload(p.s)))
+    from ._lib import STATE_BYTES, call
+
+    state = t.zeros(STATE_BYTES, dtype=t.uint8, device=dv.device())
+    call("pdas_iter_reset", dv.ptr(state), dv.stream())
+    return state
+
+
+def _fetch(state):
+    from ._lib import PdasIterState
+
+    return PdasIterState.from_buffer_copy(dv.download(state).tobytes())
+
+
+def scaling_diag(p: InteriorPoint) -> np.ndarray:
+    """d = x/s, the only iteration-dependent part of the normal equations
+    (solver.py:142-145; the engine's k_scaling kernel)."""
+    check_interior(p)
+    from ._lib import call
+
+    x, s = dv.upload(p.x), dv.upload(p.s)
+    d = dv.empty(p.x.size)
+    call("pdas_iter_scaling", dv.ptr(x), dv.ptr(s), p.x.size, dv.ptr(d),
+         dv.ptr(_state_scratch()), dv.stream())
+    return dv.download(d)
 
 
 def dir_tol(p: InteriorPoint) -> float:
@@ -219,18 +240,16 @@ def compute_directions(lp: StandardFormLP, p: InteriorPoint, backend) -> Directi
 
 def step_length(p: InteriorPoint, dirs: Directions, rho: float) -> float:
     """rho times the largest interior-preserving step; CAP_ALPHA when nothing
-    blocks (solver.py:175-189).  Ratios computed on device."""
-    t = dv.require_gpu()
+    blocks (solver.py:175-189).  The engine's ratio test (pdas_ratio_test)."""
+    from ._lib import call
+
+    n = p.x.size
     x, s = dv.upload(p.x), dv.upload(p.s)
     dx, ds = dv.upload(dirs.dx), dv.upload(dirs.ds)
-    ratios = []
-    for v, dv_ in ((x, dx), (s, ds)):
-        neg = dv_ < 0.0
-        if bool(neg.any()):
-            ratios.append(float(t.min(t.div(t.neg(v[neg]), dv_[neg])).item()))
-    if not ratios:
-        return CAP_ALPHA
-    return rho * min(ratios)
+    state = _state_scratch()
+    call("pdas_ratio_test", dv.ptr(x), dv.ptr(s), dv.ptr(dx), dv.ptr(ds), n, float(rho),
+         dv.ptr(state), dv.stream())
+    return float(_fetch(state).alpha)
 
 
 def duality_gap(p: InteriorPoint) -> float:

@@ -23,7 +23,7 @@ from _refimport import import_reference  # noqa: E402
 
 ad = import_reference()
 K = sys.modules["adascale._kernels"]
-WORKERS = os.cpu_count() or 1
+WORKERS = int(os.environ.get("GOLDEN_WORKERS", os.cpu_count() or 1))
 
 
 def sha(a) -> str:
@@ -209,7 +209,118 @@ def gen_c3():
     print("c3 it1 done", rec["t_prepare"], rec["t_iter"])
 
 
+def _blocking(p, dirs, n):
+    r = np.full(2 * n, np.inf)
+    neg = dirs.dx < 0
+    r[:n][neg] = -p.x[neg] / dirs.dx[neg]
+    neg = dirs.ds < 0
+    r[n:][neg] = -p.s[neg] / dirs.ds[neg]
+    return int(np.argmin(r)) if np.isfinite(r).any() else -1
+
+
+def gen_c5(spread=1e16, follow=2):
+    """BASELINE configs[4] / SURVEY §8(d)(ii): the ill-conditioned NEAR-OPTIMAL
+    iterate.  Runs the reference's own iteration (solver.py:222-278) on
+    gen_random_feasible(1000, 10000, 0) until max d / min d >= `spread`,
+    stores that iterate (the c5 stress point) and the next `follow`
+    iterations (dy, trace row, blocking index, iterate hashes)."""
+    m, n = 1000, 10000
+    lp, start = ad.gen_random_feasible(m, n, 0)
+    backend = ad.solver.make_backend(lp, "woodbury", WORKERS)
+    p = start.copy()
+    gap_tol = ad.solver.GAP_TOL_REL * (1.0 + abs(ad.dot_tree(lp.c, p.x)))
+    rec = {"A_sha": sha(lp.A.data), "b_sha": sha(lp.b), "c_sha": sha(lp.c),
+           "gap_tol": np.array(gap_tol), "workers": np.array(WORKERS)}
+    it, hit = 0, None
+    while True:
+        it += 1
+        d = ad.scaling_diag(p)
+        sp = float(d.max() / d.min())
+        if hit is None and sp >= spread:
+            hit = it
+            rec["start_it"] = np.array(it)  # the stored iterate is the input of iteration `it`
+            rec["start_spread"] = np.array(sp)
+            rec["x"], rec["y"], rec["s"] = p.x.copy(), p.y.copy(), p.s.copy()
+            rows, dys, blocking, shas = [], [], [], []
+        t1 = time.perf_counter()
+        dirs = ad.compute_directions(lp, p, backend)
+        alpha = ad.step_length(p, dirs, 0.9)
+        if hit is not None:
+            blocking.append(_blocking(p, dirs, n))
+            dys.append(dirs.dy.copy())
+        assert alpha < ad.solver.CAP_ALPHA
+        p.x += alpha * dirs.dx
+        p.y += alpha * dirs.dy
+        p.s += alpha * dirs.ds
+        gap = ad.duality_gap(p)
+        print(f"  c5 it {it} spread {sp:.3e} gap {gap:.3e} alpha {alpha:.6f} fallback "
+              f"{dirs.fallback} ({time.perf_counter() - t1:.1f}s)", flush=True)
+        if hit is not None:
+            rows.append([gap, alpha, ad.dot_tree(lp.c, p.x), ad.dot_tree(lp.b, p.y),
+                         dirs.residual_primal, dirs.residual_dual, dirs.residual_comp,
+                         float(dirs.fallback)])
+            shas.append([sha(p.x), sha(p.y), sha(p.s)])
+            if len(rows) == follow:
+                break
+        assert gap > gap_tol, "converged before reaching the spread"
+    rec["trace"] = np.array(rows)
+    rec["dy"] = np.array(dys)
+    rec["blocking"] = np.array(blocking)
+    rec["iter_sha"] = np.array(shas)
+    np.savez_compressed(os.path.join(HERE, "c5_nearopt.npz"), **rec)
+    print("c5 near-optimal: iterate", hit, "spread", rec["start_spread"])
+
+
+def gen_breakdown():
+    """The rare exits of solve_lp (solver.py:161-165, 226-235) on the seeded
+    instances of lp_cases.py, run through the reference's own solve_lp plus
+    the per-iteration loop (for the blocking index and iterate hashes)."""
+    import lp_cases as LC
+
+    out = {}
+    for tag, (m, n, l, seed, dl, dscale) in LC.CASES.items():
+        A, x, y, s = LC.breakdown_raw(m, n, l, seed, dl, dscale)
+        Af = ad.DenseMatrix.from_array(np.asfortranarray(A))
+        b = np.asarray(ad.mat_vec(Af, x))
+        c = np.asarray(ad.mat_t_vec(Af, y)) + s
+        lp = ad.StandardFormLP(Af, b, c)
+        start = ad.InteriorPoint(x.copy(), y.copy(), s.copy())
+        q, st, tr = ad.solve_lp(lp, start, ad.SolveOptions(workers=WORKERS))
+        # the same loop by hand: blocking index and iterate hashes per iteration
+        backend = ad.solver.make_backend(lp, "woodbury", WORKERS)
+        p = start.copy()
+        blocking, shas, cascade_ret = [], [], []
+        for it in range(len(tr)):
+            d = ad.scaling_diag(p)
+            rhs = ad.mat_vec(lp.A, p.x)
+            ws = ad.init_workspace(backend.basis, rhs)
+            cascade_ret.append(int(K.solve_sweeps(ws.cols, lp.A.as_2d(), d, ws.inner,
+                                                  ws.v_scratch, WORKERS)))
+            dirs = ad.compute_directions(lp, p, backend)
+            alpha = ad.step_length(p, dirs, 0.9)
+            blocking.append(_blocking(p, dirs, n))
+            p.x += alpha * dirs.dx
+            p.y += alpha * dirs.dy
+            p.s += alpha * dirs.ds
+            shas.append([sha(p.x), sha(p.y), sha(p.s)])
+        assert np.array_equal(p.x, q.x) and np.array_equal(p.s, q.s)
+        rows = [[r.gap, r.alpha, r.primal_obj, r.dual_obj, r.r_primal, r.r_dual,
+                 r.r_comp, float(r.fallback)] for r in tr]
+        out[f"{tag}/A_sha"] = np.array(sha(np.asfortranarray(A).ravel(order="F")))
+        out[f"{tag}/b"], out[f"{tag}/c"] = b, c
+        out[f"{tag}/status"] = np.array(st.value)
+        out[f"{tag}/trace"] = np.array(rows).reshape(len(rows), 8)
+        out[f"{tag}/blocking"] = np.array(blocking, dtype=np.int64)
+        out[f"{tag}/cascade_ret"] = np.array(cascade_ret, dtype=np.int64)
+        out[f"{tag}/iter_sha"] = np.array(shas).reshape(len(shas), 3)
+        out[f"{tag}/x"], out[f"{tag}/y"], out[f"{tag}/s"] = q.x, q.y, q.s
+        print(tag, st.value, len(tr), "fallbacks", [int(r[7]) for r in rows],
+              "cascade returns", cascade_ret)
+    np.savez_compressed(os.path.join(HERE, "breakdown.npz"), **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["kernels", "c1", "c2"]
     for w in which:
-        {"kernels": gen_kernels, "c1": gen_c1, "c2": gen_c2, "c3": gen_c3}[w]()
+        {"kernels": gen_kernels, "c1": gen_c1, "c2": gen_c2, "c3": gen_c3, "c5": gen_c5,
+         "breakdown": gen_breakdown}[w]()

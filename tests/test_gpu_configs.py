@@ -4,9 +4,10 @@ the C restatement, all host threads).
 
 * c5 (m=1000, n=10000, D spanning 1e-8..1e8 -- the fp64 stability stress):
   the whole cascade, every byte of [Y | x] and the return code.
-* c4 (m=1000, n=100000, Y ~ 800 MB): the first 256 pivots of the cascade over
-  all 100001 columns (d = 1 skips the rest, exactly as in the reference), then
-  the full 100000-step cascade twice for run-to-run bit determinism.
+* c4 (m=1000, n=100000, Y ~ 800 MB): head, middle and tail windows of 256
+  pivots in one cascade over all 100001 columns (d = 1 skips the rest, exactly
+  as in the reference), then the full 100000-step cascade twice for
+  run-to-run bit determinism.
 """
 
 import os
@@ -68,7 +69,13 @@ def test_c5_stress_cascade_bitwise(gpu):
         assert bits_equal(dv.download(dc).reshape((m, n + 1), order="F"), ref)
 
 
-def test_c4_wide_prefix_and_determinism(gpu):
+def test_c4_wide_windows_and_determinism(gpu):
+    """c4 beyond the prefix: three 256-pivot windows -- head [0, 256), middle
+    [49920, 50176) and tail [99744, 100000) (the last pivot block, the x
+    column's tile) -- active in ONE cascade over all 100001 columns, d = 1
+    (exact skips, _kernels.pyx:242-243) elsewhere; every byte of [Y | x] and
+    the return code against the reference core.  Then the full 100000-step
+    cascade twice for run-to-run bit determinism."""
     from paper_1502_03543_b200 import _device as dv
 
     m, n, k = 1000, 100000, 256
@@ -76,13 +83,17 @@ def test_c4_wide_prefix_and_determinism(gpu):
     a = np.asfortranarray(rng.uniform(-1, 1, (m, n)))
     cols = np.asfortranarray(rng.uniform(-1, 1, (m, n + 1)) / np.sqrt(m))
     d = np.power(10.0, rng.uniform(-2, 2, n))
-    dk = np.where(np.arange(n) < k, d, 1.0)
+    idx = np.arange(n)
+    live = (idx < k) | ((idx >= 49920) & (idx < 49920 + k)) | (idx >= n - k)
+    dk = np.where(live, d, 1.0)
     ref = cols.copy(order="F")
     ret = _core().solve_sweeps(ref, a, dk, np.zeros(n + 1), np.zeros(m), os.cpu_count() or 1)
     fail, dc = _gpu_cascade(cols, a, dk)
     assert fail == ret == 0
     got = dv.download(dc)
     assert bits_equal(got, ref.ravel(order="F"))
+    # the windows really moved the columns they reach
+    assert not bits_equal(ref[:, n], cols[:, n]) and bits_equal(ref[:, :1], cols[:, :1])
     del got, ref
     f1, c1 = _gpu_cascade(cols, a, d)
     h1 = dv.download(c1)

@@ -145,3 +145,33 @@ def test_restated_equals_reference_core_random():
         r1 = RESTATED.solve_sweeps(c1, a, d, i1, v1, 2)
         r2 = REFERENCE.solve_sweeps(c2, a, d, np.zeros(n + 1), np.zeros(m), 1)
         assert r1 == r2 and bits_equal(c1, c2)
+
+
+@pytest.mark.parametrize("tag", ["bd_small", "nb_small"])
+def test_oracle_rare_exits_match_reference(tag):
+    """The oracle's solve_lp on the breakdown instances (tests/golden/lp_cases.py)
+    reproduces the reference's fallback trajectory / NUMERICAL_BREAKDOWN exit
+    (tests/golden/breakdown.npz) bit for bit."""
+    import sys
+
+    from conftest import GOLDEN
+
+    sys.path.insert(0, GOLDEN)
+    import lp_cases as LC
+
+    g = load_golden("breakdown.npz")
+    m, n, l, seed, dl, dscale = LC.CASES[tag]
+    A, x, y, s = LC.breakdown_raw(m, n, l, seed, dl, dscale)
+    a = np.asfortranarray(A)
+    assert sha(a.ravel(order="F")) == str(g[f"{tag}/A_sha"])
+    K = RESTATED
+    b = K.mat_vec(a, x)
+    c = K.mat_t_vec(a, y) + s
+    assert bits_equal(b, g[f"{tag}/b"]) and bits_equal(c, g[f"{tag}/c"])
+    xo, yo, so, st, tr = O.solve_lp(K, a, b, c, x, y, s)
+    assert st.value == str(g[f"{tag}/status"])
+    rows = np.array([[r.gap, r.alpha, r.primal_obj, r.dual_obj, r.r_primal, r.r_dual, r.r_comp,
+                      float(r.fallback)] for r in tr]).reshape(len(tr), 8)
+    assert bits_equal(rows, g[f"{tag}/trace"])
+    assert [r.blocking for r in tr] == [int(v) for v in g[f"{tag}/blocking"]]
+    assert bits_equal(xo, g[f"{tag}/x"]) and bits_equal(so, g[f"{tag}/s"])
