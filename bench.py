@@ -28,8 +28,11 @@ sys.path.insert(0, REPO)
 
 M, N, SEED = 2000, 20000, 0
 METRIC = "PDAS iterations/s (m=2000, n=20000)"
+# identical in both arms (driver: same_config); what runs where goes in the
+# top-level "parallelism" / "cascade" keys
 CONFIG = {"workload": f"c3 dense LP m={M} n={N} seed={SEED} (BASELINE configs[2]), each step = "
-                      "PDAS iteration 1 from the generator's start", "m": M, "n": N}
+                      "PDAS iteration 1 from the generator's start", "m": M, "n": N,
+          "l2": "no flush: inputs larger than L2 ([Y|x] 320 MB + A 320 MB + Y 320 MB)"}
 UNIT = "iterations/s"
 
 
@@ -98,10 +101,10 @@ class ClockSampler:
 # ------------------------------------------------------------------ CPU legs
 def cascade_traffic(n, block=256):
     """DRAM bytes (read + write) of one c3 cascade, from the committed ncu
-    launch list of `tools/cascade_time.py` (profiles/r01_launches_cascade.json:
+    launch list of `tools/cascade_time.py` (profiles/r02_launches_cascade.json:
     per-kernel sums of dram__bytes_read.sum + dram__bytes_write.sum)."""
     try:
-        d = json.load(open(os.path.join(REPO, "profiles", "r01_launches_cascade.json")))
+        d = json.load(open(os.path.join(REPO, "profiles", "r02_launches_cascade.json")))
     except Exception:
         return None
     casc = {k: v for k, v in d.items() if "k_casc" in k}
@@ -155,7 +158,13 @@ def host_inputs():
 
 
 def run_reference(args):
-    """--impl reference: the reference's own compiled CPU core on this host."""
+    """--impl reference: the reference's own compiled CPU core on this host,
+    all host threads.  Each of the W + K steps is a bounded sample (cascade
+    steps 0..S-1 of iteration 1, the >99 % part of an iteration); after them
+    ONE full 20000-step cascade of iteration 1 is timed as well.  `value` is
+    the full cascade's rate (measured, not extrapolated; the rest of a
+    reference iteration is ~0.05 s); `ms_per_step` is what each
+    sample step really took, so steps x ms_per_step is the timed work."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -169,17 +178,25 @@ def run_reference(args):
         if i >= args.warmup:
             rates.append(cpu_rate(dt, es, M, N))
             times.append(dt)
-    value = float(np.median(rates))
-    sample = (f"cascade steps 0..{steps - 1} of PDAS iteration 1 at m={M}, n={N} "
-              f"(d = x0/s0), extrapolated by element-steps to the full cascade")
+    sample_rate = float(np.median(rates))
+    full_s = None
+    if not args.ref_no_full:
+        full_s, _, kind = cpu_cascade_sample(a, y, x0col, d, N, threads)
+    value = 1.0 / full_s if full_s else sample_rate
+    sample = (f"each step: cascade steps 0..{steps - 1} of PDAS iteration 1 at m={M}, n={N} "
+              f"(d = x0/s0); value: one full {N}-step cascade of that iteration, timed "
+              f"({full_s:.1f} s)" if full_s else "value extrapolated by element-steps")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(CONFIG, parallelism=f"CPU, {threads} threads"),
+        "ms_per_step": 1e3 * float(np.median(times)), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": dict(CONFIG), "parallelism": f"CPU, {threads} threads (OpenMP)",
+        "step": f"bounded sample: cascade steps 0..{steps - 1} (not a whole iteration)",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": sample, "sample_seconds": float(np.median(times))},
+                         "sample": sample, "full_cascade_s": full_s,
+                         "sample_extrapolated_value": sample_rate,
+                         "sample_seconds": float(np.median(times))},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -199,7 +216,7 @@ def run_ours(args):
 
     import paper_1502_03543_b200 as P
     from paper_1502_03543_b200 import _device as dv
-    from paper_1502_03543_b200._lib import call
+    from paper_1502_03543_b200._lib import call, load as load_lib
     from paper_1502_03543_b200.engine import DeviceProblem, DeviceSolver
 
     shard = world > 1 and args.mode == "shard"
@@ -236,6 +253,9 @@ def run_ours(args):
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = eng.launches
+    if not shard:
+        eng.time_cascade = True  # events around the cascade inside each timed step
+        eng.cascade_events.clear()
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
@@ -243,6 +263,9 @@ def run_ours(args):
             res = eng.iterate()
         ev1.record(stream)
         torch.cuda.synchronize()
+    casc_in_step = [a.elapsed_time(b) for a, b in getattr(eng, "cascade_events", [])]
+    if not shard:
+        eng.time_cascade = False
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
@@ -256,27 +279,22 @@ def run_ours(args):
     jobs = 1 if shard else world
     value = jobs * 1e3 / ms_per_step
 
-    # ---- cascade alone (dominant kernels): CUDA events on its stream
+    # ---- the dominant kernels' time: the cascade (x0 lane + panels + updates,
+    # pdas_solve_sweeps_ws_x0) timed with CUDA events on the solver's stream
+    # INSIDE the timed steps above
     m, n = M, N
-    eng.cols[:m * n].copy_(eng.basis.Y)
-    from paper_1502_03543_b200._lib import OFF_CASCADE_FAIL
+    if casc_in_step:
+        casc_s = float(np.median(casc_in_step)) / 1e3
+        casc_src = (f"median over the {len(casc_in_step)} timed steps: events around "
+                    "pdas_solve_sweeps_ws_x0 inside DeviceSolver.iterate")
+    else:  # sharded: the per-rank cascade is not one launch sequence
+        casc_s = ms_per_step / 1e3
+        casc_src = "sharded run: whole step"
+    d_it1 = eng.d.clone()  # d of iteration 1 (x0/s0), for the CPU sample
+    xcol0 = eng.rhs.clone()  # x0 = L0^-T L0^-1 (A x0)
     from paper_1502_03543_b200.engine import d_solve_many
 
-    d_it1 = eng.d.clone()  # d of iteration 1 (x0/s0)
-    xcol0 = eng.rhs.clone()  # x0 = L0^-T L0^-1 (A x0)
     d_solve_many(eng.basis.L0, m, xcol0, 1)
-    c_ms = []
-    for i in range(3):
-        eng.cols[:m * n].copy_(eng.basis.Y)
-        eng.xcol.copy_(xcol0)
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        call("pdas_solve_sweeps", dv.ptr(eng.cols), dv.ptr(prob.A), dv.ptr(d_it1), None, None,
-             m, n, 1, eng._sptr(OFF_CASCADE_FAIL), stream.cuda_stream)
-        a1.record(stream)
-        torch.cuda.synchronize()
-        c_ms.append(a0.elapsed_time(a1))
-    casc_s = float(np.median(c_ms)) / 1e3
     E, Bytes, Flops = algorithmic(m, n)
     # fp64 (separate mul/add) peak of this GPU, measured now
     sink = dv.empty(1)
@@ -302,7 +320,8 @@ def run_ours(args):
         "bound": "fp64", "achieved": achieved_tf, "peak": fp64_peak, "unit": "TFLOP/s",
         "frac": achieved_tf / fp64_peak, "traffic": cascade_traffic(N),
         "traffic_unit": "bytes per cascade (DRAM read+write of all k_casc_* launches, ncu)",
-        "traffic_source": "profiles/r01_launches_cascade.json",
+        "traffic_source": "STATIC: read from the committed ncu launch list "
+                          "profiles/r02_launches_cascade.json (not measured in this run)",
         "kernel": "cascade (k_casc_panel + k_casc_update), one 20000-step solve",
         "peak_source": "measured now: pdas_probe_fp64 (separate DMUL+DADD, no FMA)",
         "hbm_equivalent": {
@@ -313,6 +332,7 @@ def run_ours(args):
                     "element-step + pivot/A columns); frac > 1 = the register-tiled "
                     "schedule moves less than the streaming minimum"},
         "cascade_ms": casc_s * 1e3,
+        "cascade_ms_source": casc_src,
     }
 
     # ---- e2e through the public API: host iterate in, host iterate out
@@ -339,11 +359,11 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong" if shard else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": dict(CONFIG, l2="inputs larger than L2 ([Y|x] 320 MB + A + Y)",
-                       parallelism=(f"column-sharded cascade over {world} GPUs (dist.py, "
-                                    f"{args.exchange} block exchange)" if shard
-                                    else f"replicas x{world}" if world > 1 else "1 GPU"),
-                       cascade_block_pivots=128 if shard else 256),
+        "config": dict(CONFIG),
+        "parallelism": (f"column-sharded cascade over {world} GPUs (dist.py, "
+                        f"{args.exchange} block exchange)" if shard
+                        else f"replicas x{world}" if world > 1 else "1 GPU"),
+        "cascade_block_pivots": 128 if shard else int(load_lib().pdas_cascade_block_pivots()),
         "e2e": {"value": jobs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
@@ -376,7 +396,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-steps", type=int, default=1500)
-    ap.add_argument("--ref-sample-steps", type=int, default=1500)
+    ap.add_argument("--ref-sample-steps", type=int, default=1000)
+    ap.add_argument("--ref-no-full", action="store_true",
+                    help="reference arm: skip the one full-cascade timing")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--mode", default="shard", choices=["shard", "replicas"],
                     help="N>1: one LP column-sharded over the GPUs, or N independent LPs")

@@ -185,6 +185,11 @@ class DeviceSolver:
         self.state_host = t.empty(STATE_BYTES, dtype=t.uint8, pin_memory=True)
         self.dy = None
         self.launches = 0
+        # (start, end) CUDA events around each cascade on the solver's stream
+        # when time_cascade is set (bench.py: the dominant kernels' time
+        # inside the real step)
+        self.time_cascade = False
+        self.cascade_events = []
 
     # -- iterate I/O (host <-> device), the e2e boundary
     def load_iterate(self, x, y, s) -> None:
@@ -270,7 +275,13 @@ class DeviceSolver:
             B = self.basis
             self.cols[:m * n].copy_(B.Y, non_blocking=True)  # init_workspace (normal.py:121-123)
             self.xcol.copy_(self.rhs, non_blocking=True)
+            if self.time_cascade:
+                ev = (self.t.cuda.Event(enable_timing=True), self.t.cuda.Event(enable_timing=True))
+                ev[0].record(self.t.cuda.current_stream())
             self._cascade_x0()
+            if self.time_cascade:
+                ev[1].record(self.t.cuda.current_stream())
+                self.cascade_events.append(ev)
             self.dy = self.xcol
         else:
             self._solve_direct_into(self.dy_direct, self._sptr(OFF_CHOL_FAIL))

@@ -101,3 +101,34 @@ def test_c4_wide_windows_and_determinism(gpu):
     f2, c2 = _gpu_cascade(cols, a, d)
     assert f1 == f2
     assert bits_equal(dv.download(c2), h1)
+
+
+def test_c5_near_optimal_iterate_bitwise(gpu):
+    """BASELINE configs[4] as SURVEY §8(d)(ii) defines it: the reference's own
+    iterate of gen_random_feasible(1000, 10000, 0) at the first iteration
+    where max d / min d >= 1e16 (tests/golden/c5_nearopt.npz, iteration 40),
+    then two PDAS iterations on the GPU: dy, the ratio test's blocking index,
+    the trace row and the new iterate, bit for bit."""
+    from paper_1502_03543_b200 import _device as dv
+    from paper_1502_03543_b200.engine import DeviceProblem, DeviceSolver
+    from conftest import load_golden, sha
+
+    P = gpu
+    g = load_golden("c5_nearopt.npz")
+    lp, _ = P.gen_random_feasible(1000, 10000, 0)
+    assert sha(lp.A.data) == str(g["A_sha"])
+    assert sha(lp.b) == str(g["b_sha"]) and sha(lp.c) == str(g["c_sha"])
+    d = g["x"] / g["s"]
+    assert d.max() / d.min() >= 1e16
+    eng = DeviceSolver(DeviceProblem.from_lp(lp))
+    eng.load_iterate(g["x"], g["y"], g["s"])
+    for it in range(len(g["trace"])):
+        res = eng.iterate()
+        st = res.state
+        assert bits_equal(dv.download(eng.dy), g["dy"][it]), it
+        assert int(st.blocking) == int(g["blocking"][it])
+        row = [st.gap, st.alpha, st.pobj, st.dobj, st.r_primal, st.r_dual, st.r_comp,
+               float(st.fallback)]
+        assert bits_equal(np.array(row), g["trace"][it]), it
+        x, y, s = eng.read_iterate()
+        assert [sha(x), sha(y), sha(s)] == list(g["iter_sha"][it]), it
