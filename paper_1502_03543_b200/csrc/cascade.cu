@@ -43,9 +43,6 @@
 #ifndef PDAS_WS_PTRS
 #define PDAS_WS_PTRS 1
 #endif
-#ifndef PDAS_PANEL_TMA
-#define PDAS_PANEL_TMA 1
-#endif
 #ifndef PDAS_CASC_EARLYPANEL
 #define PDAS_CASC_EARLYPANEL 1
 #endif
@@ -63,6 +60,26 @@ namespace pdas {
 
 #ifndef PDAS_PANEL_TRACE
 #define PDAS_PANEL_TRACE 0
+#endif
+// Diagnostic build only (-DPDAS_HOP_TRACE=1): globaltimer marks of one panel
+// hop (tile 15 -> tile 16 of pivot block 5), read back with pdas_debug_hop_trace.
+#ifndef PDAS_HOP_TRACE
+#define PDAS_HOP_TRACE 0
+#endif
+#if PDAS_HOP_TRACE
+__device__ unsigned long long g_hop_trace[16];
+#define HOP_MARK(cond, k)                                                          \
+    do {                                                                           \
+        if ((cond) && threadIdx.x == 0) {                                          \
+            unsigned long long t_;                                                 \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+            g_hop_trace[k] = t_;                                                   \
+        }                                                                          \
+    } while (0)
+#else
+#define HOP_MARK(cond, k) \
+    do {                  \
+    } while (0)
 #endif
 #if PDAS_PANEL_TRACE
 __device__ long long g_panel_trace[8];
@@ -84,6 +101,10 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 
 __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_relaxed(int* p, int v) {
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void st_release_sys(int* p, int v) {
@@ -652,19 +673,25 @@ __device__ __forceinline__ void apply_pingpong(Tile<T, R, C, false>& tl, Pipe<S>
     pp.k += cnt;
 }
 
+// The first min(cnt, S) stages of pivots [l0, l0 + cnt) (producer thread).
+template <int S>
+__device__ __forceinline__ void apply_prologue(Pipe<S>& pp, const double* __restrict__ cols,
+                                               const double* __restrict__ a, idx_t l0, int cnt,
+                                               int m) {
+    const int pre = cnt < S ? cnt : S;
+    for (int i = 0; i < pre; ++i) pipe_issue(pp, pp.k + i, cols + (l0 + i) * m, a + (l0 + i) * m, m);
+}
+
+// issued: the caller's producer already ran apply_prologue for [l0, l1).
 template <bool TMA, int S, int T, int R, int C, bool GEN>
 __device__ __forceinline__ void apply_global(Tile<T, R, C, GEN>& tl, Pipe<S>& pp,
                                              const double* __restrict__ cols,
                                              const double* __restrict__ a, idx_t base, idx_t l0,
-                                             idx_t l1, bool producer) {
+                                             idx_t l1, bool producer, bool issued = false) {
     const int cnt = (int)(l1 - l0);
     if (cnt <= 0) return;
     const int m = tl.m;
-    if (TMA && producer) {
-        const int pre = cnt < S ? cnt : S;
-        for (int i = 0; i < pre; ++i)
-            pipe_issue(pp, pp.k + i, cols + (l0 + i) * m, a + (l0 + i) * m, m);
-    }
+    if (TMA && producer && !issued) apply_prologue(pp, cols, a, l0, cnt, m);
     // warp-uniform choice of the select-free path (every row of every lane exists)
     if (!GEN && __all_sync(0xffffffffu, tl.full()))
         apply_impl<TMA, true>(tl, pp, cols, a, base, l0, cnt, producer);
@@ -1284,7 +1311,24 @@ __device__ __forceinline__ bool panel_triangle(Tile<T, R, C, GEN>& tl, Pipe<S>& 
                                                idx_t p1, idx_t q0, int32_t* __restrict__ fail,
                                                double* bc, bool producer,
                                                double* __restrict__ cols = nullptr, idx_t n = 0,
-                                               int* __restrict__ cflags = nullptr, int epoch = 0) {
+                                               int* __restrict__ cflags = nullptr, int epoch = 0,
+                                               bool trace = false) {
+    (void)trace;
+#if PDAS_HOP_TRACE
+    long long tq = clock64();
+#define TRI_LAP(k)                                         \
+    do {                                                   \
+        if (trace && threadIdx.x == 0) {                   \
+            const long long tn = clock64();                \
+            g_hop_trace[8 + (k)] += (unsigned long long)(tn - tq); \
+            tq = tn;                                       \
+        }                                                  \
+    } while (0)
+#else
+#define TRI_LAP(k) \
+    do {           \
+    } while (0)
+#endif
     // triangle over this tile's own pivot columns, A columns via the pipe
     const int cnt = (int)((col0 + C < p1 ? col0 + C : p1) - col0);
     const unsigned k0 = pp.k;
@@ -1299,11 +1343,13 @@ __device__ __forceinline__ bool panel_triangle(Tile<T, R, C, GEN>& tl, Pipe<S>& 
             const idx_t l = col0 + cl;
             const unsigned use = k0 + cl;
             const double* ac = a + l * m;
+            TRI_LAP(5);  // chunk publication / loop overhead
             if (TMA) {
                 const int s = (int)(use % S);
                 mbar_wait(pp.full + s, (use / S) & 1u);
                 ac = pp.buf + (size_t)s * 2 * pp.mp + pp.mp;
             }
+            TRI_LAP(0);  // stage wait
             const double dl = pp.sd[l - q0];
             const bool active = dl != 1.0 && !broken;
             double part[C];
@@ -1314,6 +1360,7 @@ __device__ __forceinline__ bool panel_triangle(Tile<T, R, C, GEN>& tl, Pipe<S>& 
                 tl.publish(part, cl);
             }
             tl.sync();
+            TRI_LAP(1);  // make_v + partials + B1
             if (TMA && cl > 0) {
                 if (producer) mbar_arrive(pp.empty + (int)((use - 1) % S));
                 if (producer && cl - 1 + S < cnt)
@@ -1322,6 +1369,7 @@ __device__ __forceinline__ bool panel_triangle(Tile<T, R, C, GEN>& tl, Pipe<S>& 
             if (active) {
                 double inner[C];
                 tl.template finish<false>(part, 0.0, 0.0, inner, cl);
+                TRI_LAP(2);  // reduction + B2
                 const double denom = 1.0 + inner[cl];
                 if (fabs(denom) <= kDenomEpsRel * (1.0 + fabs(inner[cl]))) {
                     if (producer) *fail = (int32_t)(l + 1);
@@ -1341,6 +1389,7 @@ __device__ __forceinline__ bool panel_triangle(Tile<T, R, C, GEN>& tl, Pipe<S>& 
                         if (threadIdx.x > cl && threadIdx.x < C) bc[C + threadIdx.x] = bc[threadIdx.x] / denom;
                         tl.sync();
                     }
+                    TRI_LAP(3);  // denominator, divisions, B3
 #pragma unroll
                     for (int c = cl + 1; c < C; ++c) {
                         const double g = T > 32 ? bc[C + c]
@@ -1359,12 +1408,16 @@ __device__ __forceinline__ bool panel_triangle(Tile<T, R, C, GEN>& tl, Pipe<S>& 
                     }
                 }
             }
+            TRI_LAP(4);  // axpy of the later columns
             // end of a chunk: its columns are final -- store and publish them so
             // the next tile's CTA starts on them while this triangle goes on
             constexpr int CH = C / kPanelChunks > 0 ? C / kPanelChunks : 1;
             if (cflags && (cl + 1) % CH == 0 && cl + 1 < C && cl + 1 < cnt && !broken) {
+                // stores -> CTA barrier -> one gpu-scope release by the producer:
+                // the barrier orders every thread's stores before the release,
+                // which is cumulative (the cooperative-groups grid-sync pattern),
+                // so the compute threads never wait on a fence themselves
                 tl.store(cols, col0, n + 1, cl + 1 - CH, cl + 1);
-                __threadfence();
                 tl.sync();
                 if (producer) st_release(cflags + (cl + 1) / CH - 1, epoch);
             }
@@ -1414,6 +1467,10 @@ __global__ void __launch_bounds__(T, 1)
     const bool producer = threadIdx.x == 0;
     const idx_t col0 = tile * C;
     bool dead = false;
+    const bool hop_pub = gridDim.x == 32 && blockIdx.x == 15 && p0 == 5 * (p1 - p0);
+    const bool hop_con = gridDim.x == 32 && blockIdx.x == 16 && p0 == 5 * (p1 - p0);
+    (void)hop_pub;
+    (void)hop_con;
     if (uflag) {
         // this tile's last update (the update kernel of the previous block,
         // running concurrently) must have landed before the tile is read
@@ -1449,36 +1506,50 @@ __global__ void __launch_bounds__(T, 1)
         // older tiles are complete: one wait on their last chunk
         const bool prev = tp == tile - 1;
         for (int ch = prev ? 0 : NCH - 1; ch < NCH; ++ch) {
-            if (producer)
+            const idx_t pa = tp * C + (prev ? ch * CH : 0);
+            const idx_t pe = tp * C + (ch + 1) * CH;
+            const idx_t pb = pe < p1 ? pe : p1;
+            int f = 0;
+            if (producer) {
                 while (ld_acquire(flags + tp * NCH + ch) != epoch) __nanosleep(32);
+                f = *(volatile int32_t*)fail;
+                if (TMA && !f && pa < pb) {
+                    // the chunk's bulk copies go out first, so their L2 round trip
+                    // overlaps the denominators' loads below
+                    fence_proxy_async_global();  // peer CTA's generic stores -> our TMA reads
+                    apply_prologue(pp, cols, a, pa, (int)(pb - pa), m);
+                }
+            }
             // the flag's acquire and the fail word are read by one thread; the
             // barrier hands both to the CTA (block-uniform exit)
-            const int broken = __syncthreads_or(producer && *(volatile int32_t*)fail != 0);
+            const bool hop_here = hop_con && prev && ch == NCH - 1;
+            HOP_MARK(hop_here, 3);
+            const int broken = __syncthreads_or(f != 0);
             PANEL_LAP(t_wait);
             if (broken) {
                 dead = true;
                 break;
             }
-            const idx_t pa = tp * C + (prev ? ch * CH : 0);
-            const idx_t pe = tp * C + (ch + 1) * CH;
-            const idx_t pb = pe < p1 ? pe : p1;
             if (pa >= pb) continue;
             if (threadIdx.x < pb - pa) {
                 const double den = __ldcg(denoms + pa + threadIdx.x);
                 pp.sden[pa + threadIdx.x - q0] = den;
                 pp.sy[pa + threadIdx.x - q0] = div_recip(den);
             }
-            fence_proxy_async_global();  // peer CTA's generic stores -> our TMA reads
             __syncthreads();
-            apply_global<TMA>(tl, pp, cols, a, q0, pa, pb, producer);
+            HOP_MARK(hop_here, 4);
+            apply_global<TMA>(tl, pp, cols, a, q0, pa, pb, producer, true);
+            HOP_MARK(hop_here, 5);
             PANEL_LAP(t_apply);
         }
     }
     bool stored = false;
+    HOP_MARK(hop_con, 6);
     if (!dead) {
         const bool broken = panel_triangle<TMA, S, T, R, C, GEN>(
             tl, pp, a, denoms, m, col0, p1, q0, fail, bc, producer, cols, n,
-            NCH > 1 ? flags + tile * NCH : nullptr, epoch);
+            NCH > 1 ? flags + tile * NCH : nullptr, epoch, hop_con);
+        HOP_MARK(hop_pub, 0);
         if (!broken) {
             tl.store(cols, col0, n + 1);
             stored = true;
@@ -1495,8 +1566,8 @@ __global__ void __launch_bounds__(T, 1)
         }
 #endif
     }
-    __threadfence();
     __syncthreads();
+    HOP_MARK(hop_pub, 1);
     if (peers.count > 0) {
         // multi-GPU exchange fused into the panel: the tile's final columns go
         // from registers straight into every peer's [Y|x] over NVLink, with
@@ -1512,8 +1583,13 @@ __global__ void __launch_bounds__(T, 1)
         __syncthreads();
         if (producer) peer_signal(peers, fail, flags, tile * NCH + NCH - 1, epoch);
     }
-    if (producer)
-        for (int ch = 0; ch < NCH; ++ch) st_release(flags + tile * NCH + ch, epoch);
+    if (producer) {
+        // one gpu-scope fence after the CTA barrier covers every thread's stores
+        // (cumulative release); the chunk flags then go out as relaxed stores
+        __threadfence();
+        for (int ch = 0; ch < NCH; ++ch) st_relaxed(flags + tile * NCH + ch, epoch);
+    }
+    HOP_MARK(hop_pub, 2);
 }
 
 // Non-owner side of the fused exchange: wait until every tile of columns
@@ -1664,6 +1740,15 @@ struct CascOp {
     PeerSet peers{};  // kind 1 only: fused multi-GPU exchange
 };
 
+// The panel is a latency chain (one full-tile reduction per pivot step on one
+// SM), so its CTA spreads a tile over twice the update's threads (half the
+// rows per thread): each step's fp64 work and register tile halve.
+template <int T, int R>
+struct PanelShape {
+    static constexpr int TP = (R >= 2 && 2 * T <= 512) ? 2 * T : T;
+    static constexpr int RP = R * T / TP;
+};
+
 template <bool TMA, int S, int T, int R, int Cu, int G, int CT>
 static int run_cascade_impl(double* cols, const double* a, const double* d, int m, idx_t n,
                             double* denoms, int32_t* fail, int* flags, int epoch, int B,
@@ -1671,9 +1756,18 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
     constexpr bool GEN = (T == 32);
     static_assert(Cu * G == CT, "tile width");
     const size_t smem_u = casc_smem_bytes<T, Cu, G>(TMA ? S : 0, m);
-    const size_t smem_p = casc_smem_bytes<T, CT, 1>(TMA && PDAS_PANEL_TMA ? S : 0, m);
+    constexpr int TP = PanelShape<T, R>::TP, RP = PanelShape<T, R>::RP;
+    // The panel's pivot data always comes through the TMA ring when it can
+    // (prefetched S stages ahead, also where the update loads straight from
+    // L2): a latency chain cannot hide an L2 round trip per step.
+    constexpr int SP = TMA ? S : 4;
+    const bool ptma = (TMA || TP >= 128) && m % 2 == 0 &&
+                      ((uintptr_t)cols | (uintptr_t)a) % 16 == 0 &&
+                      casc_smem_bytes<TP, CT, 1>(SP, m) <= 200 * 1024;
+    const size_t smem_p = casc_smem_bytes<TP, CT, 1>(ptma ? SP : 0, m);
     auto ku = k_casc_update<TMA, S, T, R, Cu, G, GEN>;
-    auto kp = k_casc_panel<TMA && PDAS_PANEL_TMA, S, T, R, CT, GEN>;
+    auto kp = ptma ? k_casc_panel<!GEN, SP, TP, RP, CT, GEN>
+                   : k_casc_panel<false, SP, TP, RP, CT, GEN>;
     cudaFuncSetAttribute(ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_u);
     cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
     // warp-specialized update for the 256-thread single-group layouts
@@ -1694,7 +1788,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
     const idx_t ntiles = (n + 1 + CT - 1) / CT;
     if (op.kind == 1) {
         if (op.p0 % CT || op.p1 <= op.p0 || op.p1 - op.q0 > 2 * kMaxBlock) return PDAS_ERR_ARG;
-        kp<<<(unsigned)((op.p1 - op.p0 + CT - 1) / CT), T, smem_p, st>>>(
+        kp<<<(unsigned)((op.p1 - op.p0 + CT - 1) / CT), TP, smem_p, st>>>(
             cols, a, d, denoms, m, n, op.q0, op.p0, op.p1, fail, flags, epoch, nullptr, 0, op.peers);
         return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
     }
@@ -1755,7 +1849,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
             }
         }
         prof.mark(ss.ps, 1, 0, 0);
-        kp<<<(unsigned)tiles_of(0), T, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, 0, 0,
+        kp<<<(unsigned)tiles_of(0), TP, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, 0, 0,
                                                         blk_end(0), fail, flags, epoch, nullptr, 0,
                                                         PeerSet{});
         prof.mark(ss.ps, 1, 0, 1);
@@ -1788,7 +1882,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
                 const idx_t p0 = (b + 1) * B;
                 cudaStreamWaitEvent(ss.ps, ss.eU, 0);
                 prof.mark(ss.ps, 1, b + 1, 0);
-                kp<<<(unsigned)tiles_of(b + 1), T, smem_p, ss.ps>>>(
+                kp<<<(unsigned)tiles_of(b + 1), TP, smem_p, ss.ps>>>(
                     cols, a, d, denoms, m, n, p0, p0, blk_end(b + 1), fail, flags, epoch, uflag,
                     (int)(b + 1), PeerSet{});
                 prof.mark(ss.ps, 1, b + 1, 1);
@@ -1812,7 +1906,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
     cudaEventRecord(ss.e0, st);
     cudaStreamWaitEvent(ss.ps, ss.e0, 0);
     cudaEventRecord(ss.eU, st);
-    kp<<<(unsigned)tiles_of(0), T, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, 0, 0, blk_end(0),
+    kp<<<(unsigned)tiles_of(0), TP, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, 0, 0, blk_end(0),
                                                     fail, flags, epoch, nullptr, 0, PeerSet{});
     cudaEventRecord(ss.eP, ss.ps);
     for (idx_t b = 0; b < nb; ++b) {
@@ -1820,7 +1914,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         if (b + 1 < nb) {
             // panel(b+1) needs block b (stream order on ps) and U_rest(b-1)
             cudaStreamWaitEvent(ss.ps, ss.eU, 0);
-            kp<<<(unsigned)tiles_of(b + 1), T, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, b * B,
+            kp<<<(unsigned)tiles_of(b + 1), TP, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, b * B,
                                                                 (b + 1) * B, blk_end(b + 1), fail,
                                                                 flags, epoch, nullptr, 0,
                                                                 PeerSet{});
@@ -1848,19 +1942,19 @@ static int run_cascade(double* cols, const double* a, const double* d, int m, id
     // two warp-specialized CTAs per SM for the 128-thread layouts
     const size_t budget = (T == 128 ? 110 : 210) * 1024;
     if (aligned && env_int("PDAS_CASCADE_STAGES", 5) >= 5 &&
-        casc_smem_bytes<T, CT, 1>(5, m) <= budget &&
+        casc_smem_bytes<PanelShape<T, R>::TP, CT, 1>(5, m) <= budget &&
         casc_smem_bytes<T, Cu, G>(5, m) <= budget)
         return run_cascade_impl<true, 5, T, R, Cu, G, CT>(cols, a, d, m, n, denoms, fail, flags,
                                                           epoch, B, st, op);
-    if (aligned && casc_smem_bytes<T, CT, 1>(4, m) <= budget &&
+    if (aligned && casc_smem_bytes<PanelShape<T, R>::TP, CT, 1>(4, m) <= budget &&
         casc_smem_bytes<T, Cu, G>(4, m) <= budget)
         return run_cascade_impl<true, 4, T, R, Cu, G, CT>(cols, a, d, m, n, denoms, fail, flags,
                                                           epoch, B, st, op);
-    if (T == 128 && aligned && casc_smem_bytes<T, CT, 1>(3, m) <= budget &&
+    if (T == 128 && aligned && casc_smem_bytes<PanelShape<T, R>::TP, CT, 1>(3, m) <= budget &&
         casc_smem_bytes<T, Cu, G>(3, m) <= budget)
         return run_cascade_impl<true, 3, T, R, Cu, G, CT>(cols, a, d, m, n, denoms, fail, flags,
                                                           epoch, B, st, op);
-    if (aligned && casc_smem_bytes<T, CT, 1>(2, m) <= budget &&
+    if (aligned && casc_smem_bytes<PanelShape<T, R>::TP, CT, 1>(2, m) <= budget &&
         casc_smem_bytes<T, Cu, G>(2, m) <= budget)
         return run_cascade_impl<true, 2, T, R, Cu, G, CT>(cols, a, d, m, n, denoms, fail, flags,
                                                           epoch, B, st, op);
@@ -1874,6 +1968,16 @@ idx_t cascade_flags_count(idx_t m, idx_t n) { return 2 * (n + 2); }  // panel + 
 }  // namespace pdas
 extern "C" int pdas_debug_panel_trace(long long* host_out) {
     return cudaMemcpyFromSymbol(host_out, pdas::g_panel_trace, sizeof(pdas::g_panel_trace)) ==
+                   cudaSuccess
+               ? 0
+               : -2;
+}
+namespace pdas {
+#endif
+#if PDAS_HOP_TRACE
+}  // namespace pdas
+extern "C" int pdas_debug_hop_trace(unsigned long long* host_out) {
+    return cudaMemcpyFromSymbol(host_out, pdas::g_hop_trace, sizeof(pdas::g_hop_trace)) ==
                    cudaSuccess
                ? 0
                : -2;
