@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(128) k_forward(const double* __restrict__ L, i
                                                  double* __restrict__ xt) {
     extern __shared__ double smx[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const idx_t c = (idx_t)blockIdx.x * 4 + warp;
+    const idx_t c = (idx_t)blockIdx.x * (blockDim.x >> 5) + warp;
     double* xs = smx + (idx_t)warp * m;
     if (c >= k) return;
     for (idx_t i = lane; i < m; i += 32) xs[i] = x[c * m + i];
@@ -292,6 +292,59 @@ __global__ void __launch_bounds__(128) k_backward(const double* __restrict__ L, 
     }
 }
 
+// Backward substitution with each right-hand side resident in shared memory
+// (no m-fold re-read of x from global memory): warp 0, lane c, runs the serial
+// chain of right-hand side c0 + c -- for i = m-1 .. 0:
+//   s = x[i]; s -= L[j,i]*x[j] (j = i+1 .. m-1, ascending); x[i] = s / L[i,i]
+// (_kernels.pyx:186-192, the reference's exact order) -- reading x[j] from
+// shared memory (layout [row][NR], lane-contiguous) and L's column i from a
+// shared double buffer that warp 1 fills with column i-1 meanwhile.  The
+// result goes straight to column-major x (no transpose pass).
+__global__ void __launch_bounds__(64) k_backward_s(const double* __restrict__ L, idx_t m,
+                                                   const double* __restrict__ xt, idx_t k,
+                                                   double* __restrict__ x, int NR) {
+    extern __shared__ double smx[];
+    double* xs = smx;            // [m][NR]
+    double* lb = smx + m * NR;   // [2][m]: columns i (parity i & 1)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const idx_t c0 = (idx_t)blockIdx.x * NR;
+    const int nr = (int)(k - c0 < NR ? k - c0 : NR);
+    for (idx_t e = threadIdx.x; e < m * nr; e += blockDim.x) {
+        const idx_t i = e / nr, c = e % nr;
+        xs[i * NR + c] = xt[i * k + c0 + c];
+    }
+    for (idx_t j = threadIdx.x; j < m; j += blockDim.x)
+        lb[((m - 1) & 1) * m + j] = __ldg(L + (m - 1) * m + j);
+    __syncthreads();
+    for (idx_t i = m - 1; i >= 0; --i) {
+        const double* lc = lb + (i & 1) * m;
+        if (warp == 1) {
+            if (i > 0) {
+                double* nb = lb + ((i - 1) & 1) * m;
+                for (idx_t j = i - 1 + lane; j < m; j += 32) nb[j] = __ldg(L + (i - 1) * m + j);
+            }
+        } else if (lane < nr) {
+            double s = xs[i * NR + lane];
+            idx_t j = i + 1;
+            for (; j + 16 <= m; j += 16) {
+                double p[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) p[u] = lc[j + u] * xs[(j + u) * NR + lane];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) s = s - p[u];
+            }
+            for (; j < m; ++j) {
+                const double p = lc[j] * xs[j * NR + lane];
+                s = s - p;
+            }
+            xs[i * NR + lane] = s / lc[i];
+        }
+        __syncthreads();  // row i final, column i-1 staged
+    }
+    for (int c = 0; c < nr; ++c)
+        for (idx_t i = threadIdx.x; i < m; i += blockDim.x) x[(c0 + c) * m + i] = xs[i * NR + c];
+}
+
 // xt (m x k row-major) -> x (m x k column-major), 32x32 tiles.
 __global__ void k_transpose_back(const double* __restrict__ xt, idx_t m, idx_t k,
                                  double* __restrict__ x) {
@@ -317,11 +370,26 @@ int launch_solve_many(const double* low, idx_t m, double* x, idx_t k, double* wo
     if (k == 0) return PDAS_OK;
     if (k == 1 && 3 * m * (idx_t)sizeof(double) <= 200 * 1024)
         return launch_solve_one(low, m, x, work, st);
-    size_t smem = (size_t)4 * m * sizeof(double);
-    if (smem > 200 * 1024) return PDAS_ERR_UNSUPPORTED;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_forward<<<(unsigned)((k + 3) / 4), 128, smem, st>>>(low, m, x, k, work);
+    // forward: one warp per right-hand side with its x in shared memory, as many
+    // warps per CTA as fit (1 at m up to 25600)
+    constexpr size_t kSmem = 200 * 1024;
+    const size_t per = (size_t)m * sizeof(double);
+    if (per > kSmem) return PDAS_ERR_UNSUPPORTED;
+    const int wpc = (int)(kSmem / per < 4 ? kSmem / per : 4);
+    const size_t smem = (size_t)wpc * per;
+    cudaFuncSetAttribute(k_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_forward<<<(unsigned)((k + wpc - 1) / wpc), 32 * wpc, smem, st>>>(low, m, x, k, work);
+    // backward: NR right-hand sides per CTA resident in shared memory next to
+    // a double-buffered column of L; falls back to the streaming kernel when
+    // not even one fits
+    const idx_t nr = (idx_t)(kSmem / per) - 2;
+    if (nr >= 1) {
+        const int NR = (int)(nr < 32 ? nr : 32);
+        const size_t sb = ((size_t)m * NR + 2 * (size_t)m) * sizeof(double);
+        cudaFuncSetAttribute(k_backward_s, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+        k_backward_s<<<(unsigned)((k + NR - 1) / NR), 64, sb, st>>>(low, m, work, k, x, NR);
+        return PDAS_OK;
+    }
     k_backward<<<(unsigned)((k + 127) / 128), 128, 0, st>>>(low, m, work, k);
     dim3 grid((unsigned)((k + 31) / 32), (unsigned)((m + 31) / 32));
     k_transpose_back<<<grid, dim3(32, 8), 0, st>>>(work, m, k, x);

@@ -258,3 +258,17 @@ def K_solve(gpu, cols, a, d):
 
     m, n = a.shape
     return kernels.solve_sweeps(cols, a, d, np.zeros(n + 1), np.zeros(m), 1)
+
+
+@pytest.mark.parametrize("m,k", [(300, 100), (2000, 37), (2000, 1), (6500, 3), (9000, 2)])
+def test_solve_many_shared_memory_backward(K, m, k):
+    """cholesky_solve_many (_kernels.pyx:174-193): the forward sweep and the
+    shared-memory-resident backward sweep vs the oracle, including m past the
+    old 6400 limit (one resident right-hand side per CTA) and k = 1."""
+    R = O.restated()
+    rng = np.random.default_rng(m + k)
+    low = np.tril(rng.uniform(-1, 1, (m, m))) / np.sqrt(m)
+    low[np.diag_indices(m)] = rng.uniform(1.0, 2.0, m)
+    low = np.asfortranarray(low)
+    B = np.asfortranarray(rng.uniform(-1, 1, (m, k)))
+    assert bits_equal(K.cholesky_solve_many(low, B), R.cholesky_solve_many(low, B))
