@@ -139,6 +139,12 @@ class _NullBackend:
     def mark_update(self) -> None:
         pass
 
+    def block_final(self, b: int) -> None:
+        pass
+
+    def end(self) -> None:
+        pass
+
 
 def cascade_schedule(plan: ShardPlan, be) -> Iterator[Op]:
     """One sharded cascade on this rank; yields each collective (see module doc).
@@ -152,6 +158,7 @@ def cascade_schedule(plan: ShardPlan, be) -> Iterator[Op]:
         yield plan.block_op(0)
     for b in range(plan.nb):
         be.main_wait_side()  # block b is final here
+        be.block_final(b)
         if b + 1 < plan.nb:
             with be.side():
                 if plan.owns_block(b + 1):
@@ -163,6 +170,7 @@ def cascade_schedule(plan: ShardPlan, be) -> Iterator[Op]:
             be.update(*plan.block(b), i0)
         be.mark_update()
     be.main_wait_side()
+    be.end()
     if not plan.x_in_last_panel:
         yield ("x", plan.x_owner)
 
@@ -189,8 +197,18 @@ def run_collective(plan: ShardPlan, be, group=None) -> None:
             be.exchange_block(op)
         elif op[0] == "block":
             _, b, src, c0, c1, p0, p1 = op
-            for t in be.block_views(c0, c1, p0, p1):
-                dist.broadcast(t, g(src), group=group)
+            views = be.block_views(c0, c1, p0, p1)
+            pack = getattr(be, "pack_scalars", None)
+            if pack is not None:
+                # one payload for the block's columns, one for its denominators
+                # and the fail word (packed by the owner, unpacked by the rest)
+                dist.broadcast(views[0], g(src), group=group)
+                small = pack(p0, p1, src == plan.rank)
+                dist.broadcast(small, g(src), group=group)
+                be.unpack_scalars(p0, p1, small, src == plan.rank)
+            else:
+                for t in views:
+                    dist.broadcast(t, g(src), group=group)
         else:
             dist.broadcast(be.x_view(), g(op[1]), group=group)
 
@@ -233,10 +251,15 @@ class CudaShard(_NullBackend):
     updates on the caller's stream (the lookahead of the 1-GPU cascade)."""
 
     def __init__(self, plan: ShardPlan, cols, a, d, ws, fail, streams: bool = True,
-                 peers: Optional[Sequence[Tuple[int, int, int]]] = None):
+                 peers: Optional[Sequence[Tuple[int, int, int]]] = None, x0_low=None):
         """peers: for the fused exchange, (cols, ws, fail) device addresses of
         every OTHER rank, in rank order, valid in this process; None = the
-        blocks travel by broadcast (run_collective) or copy (run_lockstep)."""
+        blocks travel by broadcast (run_collective) or copy (run_lockstep).
+        x0_low: L0 -- the x0 = L0^-T L0^-1 rhs solve (normal.py:123) joins the
+        cascade: on the x column's owner it runs on its own stream (the x
+        lane) together with that tile's per-block updates, off the critical
+        path, when column n sits alone in its tile; other ranks skip it (they
+        receive x at the end).  Without an x lane the owner solves first."""
         import ctypes
 
         from . import _device as dv
@@ -262,6 +285,26 @@ class CudaShard(_NullBackend):
             self.side_stream = t.cuda.Stream(priority=hi)
             self.ev_update = t.cuda.Event()
         self.main = None
+        self.x0_low = x0_low
+        x_tile = plan.n // plan.w
+        self.xlane = (x0_low is not None and streams and not plan.x_in_last_panel
+                      and plan.rank == plan.x_owner)
+        if self.xlane:
+            # the x tile leaves the owner's regular update list
+            keep = plan.tiles[plan.tiles != x_tile]
+            self.tiles = t.from_numpy(keep.copy()).to(dv.device())
+            self._ntiles = len(keep)
+            self._starts = [int(np.searchsorted(keep, plan.tiles[plan.update_start(b)])
+                                if plan.update_start(b) < len(plan.tiles) else len(keep))
+                            for b in range(plan.nb)]
+            self.x_tiles = t.tensor([x_tile], dtype=t.int64, device=dv.device())
+            self.x_stream = t.cuda.Stream(priority=hi)
+            self.ev_block = t.cuda.Event()
+            self.x_work = t.empty(int(plan.m), dtype=t.float64, device=dv.device())
+        else:
+            self._ntiles = len(plan.tiles)
+            self._starts = None
+        self._scal = t.empty(plan.B + 1, dtype=t.float64, device=dv.device())
 
     def reset(self, cols, d):
         self.cols, self.d = cols, d
@@ -275,6 +318,34 @@ class CudaShard(_NullBackend):
             self.main = self.t.cuda.current_stream()
             self.side_stream.wait_stream(self.main)
             self.ev_update.record(self.main)
+        if self.x0_low is not None:
+            m, n = self.plan.m, self.plan.n
+            xcol = self.cols[n * m:(n + 1) * m]
+            if self.xlane:
+                self.x_stream.wait_stream(self.main)
+                with self.t.cuda.stream(self.x_stream):
+                    self.call("pdas_cholesky_solve_one", self.dv.ptr(self.x0_low), m,
+                              self.dv.ptr(xcol), self.dv.stream())
+            elif self.plan.rank == self.plan.x_owner:
+                self.call("pdas_cholesky_solve_one", self.dv.ptr(self.x0_low), m,
+                          self.dv.ptr(xcol), self.dv.stream())
+
+    def block_final(self, b: int) -> None:
+        """x lane: block b is final on the main stream -> the x tile gets it."""
+        if not self.xlane:
+            return
+        p = self.plan
+        p0, p1 = p.block(b)
+        self.ev_block.record(self.main)
+        self.x_stream.wait_event(self.ev_block)
+        with self.t.cuda.stream(self.x_stream):
+            self.call("pdas_cascade_update", self.dv.ptr(self.cols), self.dv.ptr(self.a),
+                      self.dv.ptr(self.d), p.m, p.n, p0, p1, self.dv.ptr(self.x_tiles), 1,
+                      self.dv.ptr(self.ws), self.dv.ptr(self.fail), self.dv.stream())
+
+    def end(self) -> None:
+        if self.xlane:
+            self.main.wait_stream(self.x_stream)
 
     def side(self):
         return self.t.cuda.stream(self.side_stream) if self.streams else contextlib.nullcontext()
@@ -316,9 +387,31 @@ class CudaShard(_NullBackend):
 
     def update(self, p0: int, p1: int, i0: int) -> None:
         p, dv = self.plan, self.dv
+        if self._starts is not None:  # x lane: index into the list without the x tile
+            i0 = self._starts[p0 // p.B]
+        if i0 >= self._ntiles:
+            return
         self.call("pdas_cascade_update", dv.ptr(self.cols), dv.ptr(self.a), dv.ptr(self.d), p.m,
-                  p.n, p0, p1, dv.ptr(self.tiles) + 8 * i0, len(p.tiles) - i0, dv.ptr(self.ws),
+                  p.n, p0, p1, dv.ptr(self.tiles) + 8 * i0, self._ntiles - i0, dv.ptr(self.ws),
                   dv.ptr(self.fail), dv.stream())
+
+    def pack_scalars(self, p0: int, p1: int, owner: bool):
+        """[denominators of block [p0, p1) | fail word] as one payload."""
+        sc = self._scal[: p1 - p0 + 1]
+        if owner:
+            sc[: p1 - p0].copy_(self.denoms[p0:p1])
+            sc[p1 - p0:].copy_(self._fail32().to(self.t.float64))
+        return sc
+
+    def _fail32(self):
+        # the fail word is an int32, possibly viewed as 4 bytes of the state block
+        return self.fail.view(self.t.int32) if self.fail.dtype == self.t.uint8 else self.fail
+
+    def unpack_scalars(self, p0: int, p1: int, sc, owner: bool) -> None:
+        if owner:
+            return
+        self.denoms[p0:p1].copy_(sc[: p1 - p0])
+        self._fail32().copy_(sc[p1 - p0:].to(self.t.int32))
 
     # -- collective payloads
     def block_views(self, c0, c1, p0, p1):
@@ -381,7 +474,7 @@ class ShardedSolver(DeviceSolver):
         if exchange == "peer":
             fail, peers = self._symmetric_buffers(world, rank)
         self.shard = CudaShard(self.plan, self.cols, prob.A, self.d, self.casc_ws, fail,
-                               peers=peers)
+                               peers=peers, x0_low=self.basis.L0)
         p = self.plan
         self._casc_launches = sum(1 for b in range(p.nb) if p.owns_block(b)) + sum(
             1 for b in range(p.nb) if p.update_start(b) < len(p.tiles))
@@ -432,10 +525,9 @@ class ShardedSolver(DeviceSolver):
         self.launches += self._casc_launches
 
     def _cascade_x0(self) -> None:
-        from .engine import d_solve_many
-
-        d_solve_many(self.basis.L0, self.m, self.xcol, 1)  # replicated x0 (normal.py:123)
-        self.launches += 2
+        # x0 (normal.py:123) is solved inside the schedule: on the x column's
+        # owner, on the x lane, overlapped with the cascade (CudaShard.begin)
+        self.launches += 2 if self.plan.rank == self.plan.x_owner else 0
         self._cascade()
 
 
