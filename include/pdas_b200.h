@@ -145,6 +145,8 @@ int pdas_solve_sweeps_ws_x0(double* cols, const double* a, const double* d, cons
  * p1).  No-op when *fail_dev != 0.  ws/epoch follow pdas_solve_sweeps_ws. */
 int pdas_cascade_tile_width(int64_t m);
 int pdas_cascade_block_pivots(void);
+/* Pivots per block of the 1-GPU cascade (pdas_solve_sweeps_ws / _x0). */
+int pdas_cascade_solve_block(void);
 int pdas_cascade_panel(double* cols, const double* a, const double* d, int64_t m, int64_t n,
                        int64_t q0, int64_t p0, int64_t p1, void* ws, int32_t epoch,
                        int32_t* fail_dev, void* stream);

@@ -218,7 +218,8 @@ int pdas_cascade_tile_width(int64_t m) {
     return pdas::cascade_tile_width(m);
 }
 
-int pdas_cascade_block_pivots(void) { return pdas::kCascadeBlock; }
+int pdas_cascade_block_pivots(void) { return pdas::kShardBlock; }
+int pdas_cascade_solve_block(void) { return pdas::kSolveBlock; }
 
 int64_t pdas_debug_cascade_profile(double* out, int64_t max_rows) {
     if (max_rows < 0 || (max_rows > 0 && out == nullptr)) return -1;
@@ -241,7 +242,7 @@ int pdas_cascade_panel(double* cols, const double* a, const double* d, int64_t m
         return set_err(PDAS_ERR_UNSUPPORTED, "cascade_panel: m above the compiled configurations");
     const int ct = pdas::cascade_tile_width(m);
     if (q0 < 0 || q0 > p0 || p0 >= p1 || p1 > n || p0 % ct != 0 || q0 % ct != 0 ||
-        p1 - p0 > pdas::kCascadeBlock || p0 - q0 > pdas::kCascadeBlock)
+        p1 - p0 > pdas::kShardBlock || p0 - q0 > pdas::kShardBlock)
         return set_err(PDAS_ERR_ARG, "cascade_panel: block bounds");
     double* denoms;
     int* flags;
@@ -264,7 +265,7 @@ int pdas_cascade_panel_peers(double* cols, const double* a, const double* d, int
                        "cascade_panel_peers: m above the compiled configurations");
     const int ct = pdas::cascade_tile_width(m);
     if (q0 < 0 || q0 > p0 || p0 >= p1 || p1 > n || p0 % ct != 0 || q0 % ct != 0 ||
-        p1 - p0 > pdas::kCascadeBlock || p0 - q0 > pdas::kCascadeBlock)
+        p1 - p0 > pdas::kShardBlock || p0 - q0 > pdas::kShardBlock)
         return set_err(PDAS_ERR_ARG, "cascade_panel_peers: block bounds");
     double* denoms;
     int* flags;
@@ -305,7 +306,7 @@ int pdas_cascade_update(double* cols, const double* a, const double* d, int64_t 
         return set_err(PDAS_ERR_ARG, "cascade_update: bad args");
     if (m > pdas::cascade_supported_m())
         return set_err(PDAS_ERR_UNSUPPORTED, "cascade_update: m above the compiled configurations");
-    if (p0 < 0 || p0 >= p1 || p1 > n || p1 - p0 > pdas::kCascadeBlock)
+    if (p0 < 0 || p0 >= p1 || p1 > n || p1 - p0 > pdas::kShardBlock)
         return set_err(PDAS_ERR_ARG, "cascade_update: block bounds");
     double* denoms;
     int* flags;

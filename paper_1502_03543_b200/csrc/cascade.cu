@@ -37,24 +37,6 @@
 #include "pdas_internal.h"
 #include "tma.cuh"
 
-#ifndef PDAS_WS_SADDR
-#define PDAS_WS_SADDR 1
-#endif
-#ifndef PDAS_WS_PTRS
-#define PDAS_WS_PTRS 1
-#endif
-#ifndef PDAS_CASC_EARLYPANEL
-#define PDAS_CASC_EARLYPANEL 1
-#endif
-#ifndef PDAS_HOIST_WS
-#define PDAS_HOIST_WS 0
-#endif
-#ifndef PDAS_HOIST_TRI
-#define PDAS_HOIST_TRI 0
-#endif
-#ifndef PDAS_HOIST_FIN
-#define PDAS_HOIST_FIN 1
-#endif
 
 namespace pdas {
 
@@ -312,7 +294,7 @@ struct Tile {
                 if (c < c0) continue;
                 double v = warp_butterfly(part[c], w);
                 if (GEN && H < 32) v = __shfl_sync(0xffffffffu, v, 0);
-                out[c] = DIV ? (PDAS_HOIST_FIN ? div_by(v, denom, y) : v / denom) : v;
+                out[c] = DIV ? div_by(v, denom, y) : v;
             }
         } else {
             constexpr int NW = T / 32;
@@ -336,7 +318,7 @@ struct Tile {
                 if (c >= c0 && c < C) {
                     const double u = warp_butterfly32(v[k]);
                     if (lane == 0)
-                        bc[c] = DIV ? (PDAS_HOIST_FIN ? div_by(u, denom, y) : u / denom) : u;
+                        bc[c] = DIV ? div_by(u, denom, y) : u;
                 }
             }
             sync();
@@ -377,13 +359,8 @@ struct Tile {
 // TMA bytes.  empty[s]: one arrival per consumer group once it is done.
 // `k` counts stage uses (identical in every thread of the CTA).  S (stage
 // count) is a compile-time constant so stage arithmetic is shifts/masks.
-constexpr int kMaxBlock = 256;  // pivots per block (B) upper bound
-#ifndef PDAS_PANEL_CHUNKS
-#define PDAS_PANEL_CHUNKS 2
-#endif
 // a panel tile publishes its final columns in this many chunks (flags per chunk)
-constexpr int kPanelChunks = PDAS_PANEL_CHUNKS;
-constexpr int kDefaultBlock = 256;  // 1-GPU default (c3: 2% faster than 128; dist uses 128)
+constexpr int kPanelChunks = 2;
 
 // Peers of a column-sharded cascade (dist.py): device addresses, valid in
 // this process (NVLink peer mappings), of every other rank's [Y|x], cascade
@@ -597,82 +574,6 @@ __device__ __forceinline__ void named_arrive(int id, int nthreads) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// Ping-pong schedule for two column groups sharing one pivot pipeline.
-// Each group iterates  [compute: axpy(l-1) + partials(l)] -> B1 -> reduce(l)
-// -> B2, and the compute phases of the two groups are ordered by a token
-// (named barriers 3/4, 2T threads: the finishing group arrives, the next
-// one syncs), so one group's serial reduction (shared-memory hop, shuffles,
-// the fp64 division) always runs while the other group keeps the fp64 pipe
-// busy.  Stages are recycled two pivots behind so the producer (CTA thread
-// 0, group 0) never waits on the other group's current compute phase.
-template <int S, bool FULL, int T, int R, int C>
-__device__ __forceinline__ void apply_pingpong(Tile<T, R, C, false>& tl, Pipe<S>& pp, int grp,
-                                               const double* __restrict__ cols,
-                                               const double* __restrict__ a, idx_t l0, int cnt,
-                                               bool producer) {
-    static_assert(S >= 4, "ping-pong recycles stages three pivots behind");
-    const int m = tl.m;
-    const int tok_mine = 3 + grp, tok_other = 4 - grp;
-    const double* ga = a + l0 * m;
-    const double* gc = cols + l0 * m;
-    const int stage = 2 * pp.mp;
-    const double* sd = pp.sd;  // window base == l0 in the update kernel
-    const double* sden = pp.sden;
-    if (grp == 1) named_arrive(3, 2 * T);  // group 0 computes first
-    double g[C];
-    bool prev_active = false;
-    const double* prev_pc = nullptr;
-    for (int j = 0; j <= cnt; ++j) {
-        // ---- compute phase, token-ordered between the groups
-        named_bar(tok_mine, 2 * T);
-        if (prev_active) {
-            double pl[R], ph[R];
-            tl.template load_p<false, FULL>(prev_pc, pl, ph);
-            tl.template axpy<FULL>(g, pl, ph);
-        }
-        bool active = false;
-        double part[C];
-        const double* pc = nullptr;
-        if (j < cnt) {
-            const unsigned use = pp.k + j;
-            const uint32_t s = use % S;
-            mbar_wait_a(pp.full_a + 8 * s, (use / S) & 1u);
-            pc = pp.buf + s * stage;
-            const double dl = sd[j];
-            active = dl != 1.0;
-            if (active) {
-                double vl[R], vh[R];
-                tl.template make_v<false, FULL>(pc + pp.mp, dl - 1.0, vl, vh);
-                tl.partials(vl, vh, part);
-                tl.publish(part);
-            }
-        }
-        named_arrive(tok_other, 2 * T);
-        if (j == cnt) break;
-        // ---- reduce phase
-        tl.sync();  // B1: partials published; stage of use j-1 consumed by this group
-        if (j >= 2) {
-            const unsigned done = pp.k + j - 2;  // released two pivots behind
-            if (tl.t == 0) mbar_arrive_a(pp.empty_a + 8 * (done % S));
-        }
-        // refill three behind: the other group released that use an iteration ago
-        if (producer && j >= 3 && j - 3 + S < cnt)
-            pipe_issue(pp, pp.k + j - 3 + S, gc + (size_t)(j - 3 + S) * m,
-                       ga + (size_t)(j - 3 + S) * m, m);
-        if (active) tl.template finish<true>(part, sden[j], pp.sy[j], g);
-        prev_active = active;
-        prev_pc = pc;
-    }
-    if (grp == 0) named_bar(3, 2 * T);  // consume group 1's last token
-    // release the last two uses (j = cnt-2, cnt-1) once this group is done
-    tl.sync();
-    if (tl.t == 0) {
-        for (int j = cnt - 2 > 0 ? cnt - 2 : 0; j < cnt; ++j)
-            mbar_arrive_a(pp.empty_a + 8 * ((pp.k + j) % S));
-    }
-    pp.k += cnt;
-}
-
 // The first min(cnt, S) stages of pivots [l0, l0 + cnt) (producer thread).
 template <int S>
 __device__ __forceinline__ void apply_prologue(Pipe<S>& pp, const double* __restrict__ cols,
@@ -712,26 +613,10 @@ __device__ __forceinline__ void apply_global(Tile<T, R, C, GEN>& tl, Pipe<S>& pp
 // v_j and P_j are carried in registers between the two uses; stage j is
 // recycled by the producer once PA(j+1) shows its last reader finished.
 // Named barriers (384 threads): 1 = PA, 2 = PB, 3 = GA, 4 = GB.
-#ifndef PDAS_ISSUE_LATE
-#define PDAS_ISSUE_LATE 1
-#endif
-#ifndef PDAS_PREFETCH_ACT
-#define PDAS_PREFETCH_ACT 1
-#endif
-#ifndef PDAS_WS_LDG
-#define PDAS_WS_LDG 1
-#endif
 constexpr int kWsT = 256;       // compute threads
-constexpr int kWsThreads = 384; // + reducer warpgroup
 // compute 224 / reducer 56 (c3 -0.9% vs 232 / 40: the reducer keeps its pivot scalars and
 // addresses in registers; the compute tile still fits without spills)
-#ifndef PDAS_WS_REGS_R
-#define PDAS_WS_REGS_R 56
-#endif
-#ifndef PDAS_WS_REGS_C
-#define PDAS_WS_REGS_C 224
-#endif
-constexpr int kWsRegsCompute = PDAS_WS_REGS_C, kWsRegsReducer = PDAS_WS_REGS_R;
+constexpr int kWsRegsCompute = 224, kWsRegsReducer = 56;
 
 // Diagnostic build only (make variant VDEFS=-DPDAS_WS_TRACE=1): clock64 marks
 // of compute thread 0 / reducer thread 0 of one CTA per pivot, read back with
@@ -809,11 +694,9 @@ __device__ __forceinline__ void ws_compute(Tile<TC, R, C, false>& tl, const doub
     const double* st_cur = buf;
     const double* st_nxt = S > 1 ? buf + stage : buf;
     for (int j = 0; j < cnt; ++j) {
-#if PDAS_PREFETCH_ACT
         // d of pivot j+1, read before the barriers it would otherwise follow
         const double dn = sd[j + 1 < cnt ? j + 1 : j];
         const bool a_next = j + 1 < cnt && dn != 1.0;
-#endif
         // ---- C1(j)
         WS_MARK(0, j, 0);
         if (j > 0) {
@@ -827,10 +710,6 @@ __device__ __forceinline__ void ws_compute(Tile<TC, R, C, false>& tl, const doub
         // ---- C2(j)
         named_bar(3, NT);  // gA(j) ready, stage j+1 ready
         WS_MARK(0, j, 3);
-#if !PDAS_PREFETCH_ACT
-        const double dn = sd[j + 1 < cnt ? j + 1 : j];
-        const bool a_next = j + 1 < cnt && dn != 1.0;
-#endif
         if (a_cur) {
             tl.template load_p<false, FULL>(st_cur, pl, ph);
             axpy(0, bcA);
@@ -865,14 +744,12 @@ __device__ __forceinline__ void ws_compute_ldg(Tile<TC, R, C, false>& tl,
     constexpr int HC = C / 2, NT = TC + 128;
     double vl[R], vh[R], pl[R], ph[R];
     double npl[R], nph[R], nal[R], nah[R];  // P_{j+1}, raw A_{j+2} in flight
-#if PDAS_WS_SADDR
     // 32-bit shared addresses computed once and made opaque, so the loop
     // does not rebuild the shared window base (S2UR/ULEA) and the thread
     // index (S2R) for every reduction store and multiplier load
     const uint32_t sa_red[2] = {opaque_u32(smem_addr(redA + tl.t)),
                                 opaque_u32(smem_addr(redB + tl.t))};
     const uint32_t sa_bc[2] = {opaque_u32(smem_addr(bcA)), opaque_u32(smem_addr(bcB))};
-#endif
     auto partials = [&](int h0, double* red) {
 #pragma unroll
         for (int c = 0; c < HC; ++c) {
@@ -883,16 +760,11 @@ __device__ __forceinline__ void ws_compute_ldg(Tile<TC, R, C, false>& tl,
                 double hi = vh[r] * tl.xh[r][h0 + c];
                 s[r] = lo + hi;
             }
-#if PDAS_WS_SADDR
             st_shared_f64(sa_red[h0 ? 1 : 0] + 8u * (uint32_t)(c * TC), lane_tree<R>(s));
-#else
-            red[c * TC + tl.t] = lane_tree<R>(s);
-#endif
         }
     };
     auto axpy = [&](int h0, const double* bc) {
         double g[HC];
-#if PDAS_WS_SADDR
         if constexpr (HC % 2 == 0) {
 #pragma unroll
             for (int c = 0; c < HC; c += 2)
@@ -901,10 +773,6 @@ __device__ __forceinline__ void ws_compute_ldg(Tile<TC, R, C, false>& tl,
 #pragma unroll
             for (int c = 0; c < HC; ++c) g[c] = bc[c];
         }
-#else
-#pragma unroll
-        for (int c = 0; c < HC; ++c) g[c] = bc[c];
-#endif
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const bool hi = FULL || tl.vhi(r);
@@ -929,7 +797,6 @@ __device__ __forceinline__ void ws_compute_ldg(Tile<TC, R, C, false>& tl,
             vh[r] = (FULL || tl.vhi(r)) ? nah[r] * f : 0.0;
         }
     };
-#if PDAS_WS_PTRS
     // loop-carried per-thread column pointers (this thread's first row folded
     // in): the loads need no per-pivot address rebuild (S2R/LDC chains the
     // compiler otherwise rematerialises under register pressure)
@@ -943,7 +810,6 @@ __device__ __forceinline__ void ws_compute_ldg(Tile<TC, R, C, false>& tl,
     };
     const double* pnext = pcol + m + tl.t;
     const double* anext = acol + 2 * (size_t)m + tl.t;
-#endif
     // prologue: v_0, P_0 and A_1 in registers / in flight
     tl.template load_p<true, FULL>(acol, nal, nah);
     tl.template load_p<true, FULL>(pcol, npl, nph);
@@ -952,12 +818,7 @@ __device__ __forceinline__ void ws_compute_ldg(Tile<TC, R, C, false>& tl,
     if (cnt > 1) tl.template load_p<true, FULL>(acol + m, nal, nah);
     if (a_cur) partials(0, redA);
     named_arrive(1, NT);
-#ifndef PDAS_WS_UNROLL2
-#define PDAS_WS_UNROLL2 1
-#endif
-#if PDAS_WS_UNROLL2
 #pragma unroll 2
-#endif
     for (int j = 0; j < cnt; ++j) {
         const double dn = sd[j + 1 < cnt ? j + 1 : j];
         const bool a_next = j + 1 < cnt && dn != 1.0;
@@ -979,20 +840,12 @@ __device__ __forceinline__ void ws_compute_ldg(Tile<TC, R, C, false>& tl,
             pl[r] = npl[r];
             ph[r] = nph[r];
         }
-#if PDAS_WS_PTRS
         if (j + 1 < cnt) ldp(pnext, npl, nph);
         pnext += m;
-#else
-        if (j + 1 < cnt) tl.template load_p<true, FULL>(pcol + (size_t)(j + 1) * m, npl, nph);
-#endif
         if (a_cur) axpy(0, bcA);
         scale(dn - 1.0);
-#if PDAS_WS_PTRS
         if (j + 2 < cnt) ldp(anext, nal, nah);
         anext += m;
-#else
-        if (j + 2 < cnt) tl.template load_p<true, FULL>(acol + (size_t)(j + 2) * m, nal, nah);
-#endif
         if (a_next) partials(0, redA);
         named_arrive(1, NT);
         WS_MARK(0, j, 4);
@@ -1029,13 +882,12 @@ __device__ __forceinline__ void ws_reducer_ldg(const double* sd, const double* s
             const int c = w + 4 * k;
             if (c < HC) {
                 const double u = warp_butterfly32(v[k]);
-                const double g = PDAS_HOIST_WS ? div_by(u, denom, y) : u / denom;
+                const double g = u / denom;
                 if (lane == 0) bc[c] = g;
             }
         }
     };
-#if PDAS_WS_SADDR
-    if constexpr (HC <= 4 && !PDAS_HOIST_WS && !PDAS_WS_TRACE) {
+    if constexpr (HC <= 4 && !PDAS_WS_TRACE) {
         // one column per warp: its reduction rows, its multiplier slot and the
         // pivot scalars as pinned 32-bit shared addresses (no per-pivot
         // shared-window rebuild, as in ws_compute_ldg)
@@ -1072,7 +924,6 @@ __device__ __forceinline__ void ws_reducer_ldg(const double* sd, const double* s
         named_bar(1, NT);  // the compute warps' final PA arrival
         return;
     }
-#endif
     bool act = sd[0] != 1.0;
     double den = sden[0], y = sy[0];
     for (int j = 0; j < cnt; ++j) {
@@ -1104,7 +955,7 @@ __device__ __forceinline__ void ws_reducer(Pipe<S>& pp, const double* __restrict
                                            const double* redA, const double* redB, double* bcA,
                                            double* bcB) {
     constexpr int HC = C / 2, NT = TC + 128, NW = TC / 32;
-    constexpr bool kLateIssue = PDAS_ISSUE_LATE && S >= 3;
+    constexpr bool kLateIssue = S >= 3;
     const int rt = threadIdx.x - TC;  // 0..127
     const int w = rt >> 5, lane = rt & 31;
     const bool producer = rt == 0;
@@ -1133,7 +984,7 @@ __device__ __forceinline__ void ws_reducer(Pipe<S>& pp, const double* __restrict
             const int c = w + 4 * k;
             if (c < HC) {
                 const double u = warp_butterfly32(v[k]);
-                const double g = PDAS_HOIST_WS ? div_by(u, denom, y) : u / denom;
+                const double g = u / denom;
                 if (lane == 0) bc[c] = g;
             }
         }
@@ -1202,7 +1053,7 @@ __global__ void __launch_bounds__(TC + 128, TC == 128 ? 2 : 1)
                      const int64_t* __restrict__ tiles, int* __restrict__ uflag, int utag,
                      int ucount) {
     static_assert(TC == 256 || TC == 128, "compute threads");
-    constexpr bool kLdg = PDAS_WS_LDG && R <= 4;
+    constexpr bool kLdg = R <= 4;
     constexpr int kRegC = TC == 256 ? kWsRegsCompute : (kLdg ? 208 : 216);
     constexpr int kRegR = TC == 256 ? kWsRegsReducer : (kLdg ? 48 : 40);
     double *red, *bc;
@@ -1278,18 +1129,7 @@ __global__ void __launch_bounds__(T* G, 1)
     const idx_t tile = tiles ? tiles[blockIdx.x] : tile0 + blockIdx.x;
     const idx_t col0 = tile * (C * G) + grp * C;
     tl.load(cols, col0, n + 1);
-    if constexpr (TMA && G == 2 && !GEN && S >= 4) {
-        const int cnt = (int)(p1 - p0);
-        if (threadIdx.x == 0)
-            for (int i = 0; i < (cnt < S ? cnt : S); ++i)
-                pipe_issue(pp, pp.k + i, cols + (p0 + i) * m, a + (p0 + i) * m, m);
-        if (__all_sync(0xffffffffu, tl.full()))
-            apply_pingpong<S, true>(tl, pp, grp, cols, a, p0, cnt, threadIdx.x == 0);
-        else
-            apply_pingpong<S, false>(tl, pp, grp, cols, a, p0, cnt, threadIdx.x == 0);
-    } else {
-        apply_global<TMA>(tl, pp, cols, a, p0, p0, p1, threadIdx.x == 0);
-    }
+    apply_global<TMA>(tl, pp, cols, a, p0, p0, p1, threadIdx.x == 0);
     tl.store(cols, col0, n + 1);
     if (uflag && (int)blockIdx.x < ucount) {
         __threadfence();
@@ -1376,7 +1216,6 @@ __device__ __forceinline__ bool panel_triangle(Tile<T, R, C, GEN>& tl, Pipe<S>& 
                     broken = true;
                 } else {
                     if (producer) denoms[l] = denom;
-                    const double yd = div_recip(denom);
                     double pl[R], ph[R];
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
@@ -1393,7 +1232,7 @@ __device__ __forceinline__ bool panel_triangle(Tile<T, R, C, GEN>& tl, Pipe<S>& 
 #pragma unroll
                     for (int c = cl + 1; c < C; ++c) {
                         const double g = T > 32 ? bc[C + c]
-                                         : (PDAS_HOIST_TRI ? div_by(inner[c], denom, yd) : inner[c] / denom);
+                                         : inner[c] / denom;
 #pragma unroll
                         for (int r = 0; r < R; ++r) {
                             if (tl.vlo(r)) {
@@ -1523,6 +1362,7 @@ __global__ void __launch_bounds__(T, 1)
             // the flag's acquire and the fail word are read by one thread; the
             // barrier hands both to the CTA (block-uniform exit)
             const bool hop_here = hop_con && prev && ch == NCH - 1;
+            (void)hop_here;
             HOP_MARK(hop_here, 3);
             const int broken = __syncthreads_or(f != 0);
             PANEL_LAP(t_wait);
@@ -1618,17 +1458,12 @@ static int env_int(const char* name, int dflt) {
 
 static CascCfg cascade_cfg(idx_t m) {
     const idx_t H = m > 1 ? pow2_ceil(m) >> 1 : 0;
-    const int variant = env_int("PDAS_CASCADE_VARIANT", 0);
     if (H <= 32) return {32, 1, 8, 1, 8};
     if (H == 64) return {64, 1, 8, 1, 8};
     if (H == 128) return {128, 1, 8, 1, 8};
-    if (H == 256)  // 2 WS CTAs per SM; variant 3: the 512-thread ping-pong layout
-        return variant == 3 ? CascCfg{256, 1, 8, 2, 16} : CascCfg{128, 2, 8, 1, 8};
-    if (H == 512)
-        return variant == 1   ? CascCfg{256, 2, 8, 2, 16}
-               : variant == 2 ? CascCfg{256, 2, 16, 1, 16}
-                              : CascCfg{128, 4, 8, 1, 8};  // 2 WS CTAs per SM
-    if (H == 1024) return variant == 1 ? CascCfg{256, 4, 4, 2, 8} : CascCfg{256, 4, 8, 1, 8};
+    if (H == 256) return {128, 2, 8, 1, 8};   // 2 warp-specialized CTAs per SM
+    if (H == 512) return {128, 4, 8, 1, 8};   // 2 warp-specialized CTAs per SM
+    if (H == 1024) return {256, 4, 8, 1, 8};  // warp-specialized, 1 CTA per SM
     if (H == 2048) return {256, 8, 4, 1, 4};
     if (H == 4096) return {256, 16, 2, 1, 2};
     if (H == 8192) return {256, 32, 1, 1, 1};
@@ -1782,7 +1617,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
     const int ws_threads = TCW + 128;
     auto kws = k_casc_update_ws<S, RW, CW, TCW>;
     const size_t smem_ws = casc_smem_bytes<TCW, CW, 1>(S, m);
-    const bool use_ws = kUseWs && env_int("PDAS_CASCADE_WS", 1) != 0;
+    constexpr bool use_ws = kUseWs;
     if (use_ws)
         cudaFuncSetAttribute(kws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ws);
     const idx_t ntiles = (n + 1 + CT - 1) / CT;
@@ -1807,18 +1642,8 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
     const idx_t nb = (n + B - 1) / B;
     auto blk_end = [&](idx_t b) { return (b + 1) * B < n ? (b + 1) * B : n; };
     auto tiles_of = [&](idx_t b) { return (blk_end(b) - b * B + CT - 1) / CT; };
-    auto update = [&](idx_t b, idx_t t0, int* uf) {
-        if (t0 >= ntiles) return;
-        const int uc = uf && b + 1 < nb ? (int)tiles_of(b + 1) : 0;
-        if (use_ws)
-            kws<<<(unsigned)(ntiles - t0), ws_threads, smem_ws, st>>>(
-                cols, a, d, denoms, m, n, b * B, blk_end(b), t0, fail, nullptr, uf, (int)(b + 1), uc);
-        else
-            ku<<<(unsigned)(ntiles - t0), T * G, smem_u, st>>>(
-                cols, a, d, denoms, m, n, b * B, blk_end(b), t0, fail, nullptr, uf, (int)(b + 1), uc);
-    };
     SideStream& ss = side_stream();
-    if (PDAS_CASC_EARLYPANEL) {
+    {
         // U(b) covers block b+1's tiles too (its lowest CTAs) and flags each
         // tile as it lands; panel(b+1) -- only the block's own chain and
         // triangle -- waits on those flags inside the kernel, so it starts as
@@ -1903,29 +1728,6 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         prof.finish(st);
         return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
     }
-    cudaEventRecord(ss.e0, st);
-    cudaStreamWaitEvent(ss.ps, ss.e0, 0);
-    cudaEventRecord(ss.eU, st);
-    kp<<<(unsigned)tiles_of(0), TP, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, 0, 0, blk_end(0),
-                                                    fail, flags, epoch, nullptr, 0, PeerSet{});
-    cudaEventRecord(ss.eP, ss.ps);
-    for (idx_t b = 0; b < nb; ++b) {
-        cudaStreamWaitEvent(st, ss.eP, 0);  // panel(b): block b is final
-        if (b + 1 < nb) {
-            // panel(b+1) needs block b (stream order on ps) and U_rest(b-1)
-            cudaStreamWaitEvent(ss.ps, ss.eU, 0);
-            kp<<<(unsigned)tiles_of(b + 1), TP, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, b * B,
-                                                                (b + 1) * B, blk_end(b + 1), fail,
-                                                                flags, epoch, nullptr, 0,
-                                                                PeerSet{});
-            cudaEventRecord(ss.eP, ss.ps);
-        }
-        // U_rest(b): every tile beyond block b+1 (or beyond block b at the end)
-        const idx_t last = b + 1 < nb ? blk_end(b + 1) : blk_end(b);
-        update(b, (last + CT - 1) / CT, nullptr);
-        cudaEventRecord(ss.eU, st);
-    }
-    return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
 }
 
 template <int T, int R, int Cu, int G, int CT>
@@ -1941,7 +1743,7 @@ static int run_cascade(double* cols, const double* a, const double* d, int m, id
                          (((uintptr_t)cols | (uintptr_t)a) % 16 == 0);
     // two warp-specialized CTAs per SM for the 128-thread layouts
     const size_t budget = (T == 128 ? 110 : 210) * 1024;
-    if (aligned && env_int("PDAS_CASCADE_STAGES", 5) >= 5 &&
+    if (aligned &&
         casc_smem_bytes<PanelShape<T, R>::TP, CT, 1>(5, m) <= budget &&
         casc_smem_bytes<T, Cu, G>(5, m) <= budget)
         return run_cascade_impl<true, 5, T, R, Cu, G, CT>(cols, a, d, m, n, denoms, fail, flags,
@@ -2010,11 +1812,7 @@ static int dispatch_cascade(double* cols, const double* a, const double* d, idx_
     PDAS_CASC(128, 1, 8, 1, 8)
     PDAS_CASC(128, 4, 8, 1, 8)
     PDAS_CASC(128, 2, 8, 1, 8)
-    PDAS_CASC(256, 1, 8, 2, 16)
-    PDAS_CASC(256, 2, 8, 2, 16)
     PDAS_CASC(256, 4, 8, 1, 8)
-    PDAS_CASC(256, 4, 4, 2, 8)
-    PDAS_CASC(256, 2, 16, 1, 16)
     PDAS_CASC(256, 8, 4, 1, 4)
     PDAS_CASC(256, 16, 2, 1, 2)
     PDAS_CASC(256, 32, 1, 1, 1)
@@ -2028,7 +1826,7 @@ int launch_cascade(double* cols, const double* a, const double* d, idx_t m, idx_
     if (m < 1 || n < 0 || m > INT_MAX / 4) return PDAS_ERR_ARG;
     cudaMemsetAsync(fail_dev, 0, sizeof(int32_t), st);
     if (n == 0) return PDAS_OK;
-    const int B = block_pivots > 0 ? block_pivots : env_int("PDAS_CASCADE_BLOCK", kDefaultBlock);
+    const int B = block_pivots > 0 ? block_pivots : kSolveBlock;
     return dispatch_cascade(cols, a, d, m, n, denoms, fail_dev, flags, epoch, B, st, CascOp{});
 }
 
@@ -2041,13 +1839,8 @@ int launch_cascade_x0(double* cols, const double* a, const double* d, const doub
     CascOp op;
     op.x0_low = low;
     op.x0_work = work;
-    const int B = env_int("PDAS_CASCADE_BLOCK", kDefaultBlock);
-    if (!PDAS_CASC_EARLYPANEL) {  // the x lane exists in the early-panel schedule only
-        int rc = launch_solve_one(low, m, cols + (size_t)n * m, work, st);
-        if (rc) return rc;
-        op = CascOp{};
-    }
-    return dispatch_cascade(cols, a, d, m, n, denoms, fail_dev, flags, epoch, B, st, op);
+    return dispatch_cascade(cols, a, d, m, n, denoms, fail_dev, flags, epoch, kSolveBlock, st,
+                            op);
 }
 
 int launch_cascade_panel(double* cols, const double* a, const double* d, idx_t m, idx_t n,

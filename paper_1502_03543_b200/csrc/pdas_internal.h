@@ -95,7 +95,14 @@ idx_t cascade_supported_m();
 idx_t cascade_flags_count(idx_t m, idx_t n);
 int cascade_tile_width(idx_t m);
 idx_t cascade_profile_rows(double* out, idx_t max_rows);
-constexpr int kCascadeBlock = 128;  // pivots per block (= kMaxBlock in cascade.cu)
+// Pivot blocks (B, pivots per panel/update round): the 1-GPU cascade uses
+// kSolveBlock (pdas_cascade_solve_block), the sharded building blocks of
+// dist.py kShardBlock (pdas_cascade_block_pivots: a shorter panel per
+// exchange); kernels size their shared scalar windows for kMaxBlock.
+constexpr int kMaxBlock = 256;
+constexpr int kSolveBlock = 256;  // c3: 2 % faster than 128 (per-tile reload, launches)
+constexpr int kShardBlock = 128;
+static_assert(kSolveBlock <= kMaxBlock && 2 * kShardBlock <= 2 * kMaxBlock, "block sizes");
 
 // solve_kernels.cu (single right-hand side, latency-optimised)
 int launch_solve_one(const double* low, idx_t m, double* x, double* work, cudaStream_t st);

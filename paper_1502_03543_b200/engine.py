@@ -17,7 +17,6 @@ PCIe bus per iteration; the SingularUpdate fallback to the direct solve
 
 from __future__ import annotations
 
-import os
 import time
 
 import numpy as np
@@ -258,7 +257,7 @@ class DeviceSolver:
              dv.ptr(self.basis.L0), m, n, dv.ptr(self.casc_ws), self.epoch,
              self._sptr(OFF_CASCADE_FAIL), dv.stream())
         # x0 solve (2) + per pivot block: panel, update, and the x lane's update
-        blk = int(os.environ.get("PDAS_CASCADE_BLOCK", "256"))
+        blk = int(load().pdas_cascade_solve_block())
         xlane = n % int(load().pdas_cascade_tile_width(m)) == 0
         self.launches += 2 + (3 if xlane else 2) * ((n + blk - 1) // blk)
 

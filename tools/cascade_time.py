@@ -3,8 +3,7 @@
     python tools/cascade_time.py [--m 2000 --n 20000 --reps 3]
 
 Inputs are synthetic ([Y | x] random, d = 10^U[-1,1]); the cascade's cost
-does not depend on the values.  Honours PDAS_CASCADE_VARIANT /
-PDAS_CASCADE_BLOCK (read by the library at launch)."""
+does not depend on the values."""
 import argparse
 import ctypes
 import os
@@ -46,5 +45,4 @@ for rep in range(args.reps + 1):
     if rep:
         print(f"m={m} n={n} cascade {ms:.2f} ms  {4 * E / ms / 1e9:.2f} TFLOP/s  "
               f"{16 * E / ms / 1e6:.0f} GB/s-equiv  fail={int(fail.item())}  "
-              f"variant={os.environ.get('PDAS_CASCADE_VARIANT', '0')} "
-              f"B={os.environ.get('PDAS_CASCADE_BLOCK', '256')}", flush=True)
+              f"B={int(load().pdas_cascade_solve_block())}", flush=True)
