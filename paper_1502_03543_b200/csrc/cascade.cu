@@ -81,6 +81,12 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
     return v;
 }
 
+__device__ __forceinline__ int ld_acquire_(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -97,6 +103,25 @@ __device__ __forceinline__ int ld_acquire_sys(const int* p) {
     int v;
     asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+
+int panel_flag_chunks(int ct);
+
+// Dependencies of an update CTA that may start before the previous update
+// kernel has finished (programmatic dependent launch, run_cascade_impl):
+//   * the block's panel is complete: its last tile's last chunk flag (pflag)
+//     carries this cascade's epoch;
+//   * this tile has received the previous block: tile_done[tile] >= need.
+// One thread spins; the caller's barrier hands the result to the CTA.
+__device__ __forceinline__ void update_deps(const int* pflag, int epoch, const int* tile_done,
+                                            idx_t tile, int need, const int32_t* fail) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (threadIdx.x != 0) return;
+    if (pflag)
+        while (*(volatile const int32_t*)fail == 0 && ld_acquire_(pflag) != epoch) __nanosleep(64);
+    if (tile_done && need > 0)
+        while (*(volatile const int32_t*)fail == 0 && ld_acquire_(tile_done + tile) < need)
+            __nanosleep(64);
 }
 
 // a value the compiler must keep in a register (it cannot rematerialise it)
@@ -1051,7 +1076,7 @@ __global__ void __launch_bounds__(TC + 128, TC == 128 ? 2 : 1)
                      const double* __restrict__ d, const double* __restrict__ denoms, int m,
                      idx_t n, idx_t p0, idx_t p1, idx_t tile0, const int32_t* __restrict__ fail,
                      const int64_t* __restrict__ tiles, int* __restrict__ uflag, int utag,
-                     int ucount) {
+                     int need, const int* __restrict__ pflag, int epoch) {
     static_assert(TC == 256 || TC == 128, "compute threads");
     constexpr bool kLdg = R <= 4;
     constexpr int kRegC = TC == 256 ? kWsRegsCompute : (kLdg ? 208 : 216);
@@ -1063,6 +1088,9 @@ __global__ void __launch_bounds__(TC + 128, TC == 128 ? 2 : 1)
         for (int s = 0; s < S; ++s) mbar_init(pp.full + s, 1);
         mbar_fence_init();
     }
+    const idx_t tile = tiles ? tiles[blockIdx.x] : tile0 + blockIdx.x;
+    update_deps(pflag, epoch, uflag, tile, need, fail);
+    __syncthreads();
     stage_scalars(pp, d, denoms, p0, p0, p1, true);
     // a breakdown found by a concurrent panel: one thread reads the fail word and
     // the whole CTA leaves together (before setmaxnreg and the barrier protocol)
@@ -1084,7 +1112,7 @@ __global__ void __launch_bounds__(TC + 128, TC == 128 ? 2 : 1)
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegC));
     Tile<TC, R, C, false> tl;
     tl.init(threadIdx.x, m, 0, red, bc);
-    const idx_t col0 = (tiles ? tiles[blockIdx.x] : tile0 + blockIdx.x) * C;
+    const idx_t col0 = tile * C;
     tl.load(cols, col0, n + 1);
     const bool full = __all_sync(0xffffffffu, tl.full());
     if constexpr (kLdg) {
@@ -1101,7 +1129,7 @@ __global__ void __launch_bounds__(TC + 128, TC == 128 ? 2 : 1)
             ws_compute<S, R, C, false, TC>(tl, pp.buf, pp.mp, pp.sd, cnt, redA, redB, bcA, bcB);
     }
     tl.store(cols, col0, n + 1);
-    if (uflag && (int)blockIdx.x < ucount) {  // tile done: the next panel may take it
+    if (uflag) {  // tile done: the next panel and the next update may take it
         __threadfence();
         named_bar(5, TC);
         if (threadIdx.x == 0) st_release(uflag + col0 / C, utag);
@@ -1117,21 +1145,23 @@ __global__ void __launch_bounds__(T* G, 1)
                   const double* __restrict__ d, const double* __restrict__ denoms, int m, idx_t n,
                   idx_t p0, idx_t p1, idx_t tile0, const int32_t* __restrict__ fail,
                   const int64_t* __restrict__ tiles, int* __restrict__ uflag, int utag,
-                     int ucount) {
+                  int need, const int* __restrict__ pflag, int epoch) {
     double *red, *bc;
     Pipe<S> pp;
     carve<T, C, G, S>(red, bc, pp, TMA, m);
+    const idx_t tile = tiles ? tiles[blockIdx.x] : tile0 + blockIdx.x;
+    update_deps(pflag, epoch, uflag, tile, need, fail);
+    __syncthreads();
     stage_scalars(pp, d, denoms, p0, p0, p1, true);
     if (__syncthreads_or(threadIdx.x == 0 && *(volatile const int32_t*)fail != 0)) return;
     const int grp = threadIdx.x / T;
     Tile<T, R, C, GEN> tl;
     tl.init(threadIdx.x % T, m, 1 + grp, red + grp * C * T, bc + grp * C);
-    const idx_t tile = tiles ? tiles[blockIdx.x] : tile0 + blockIdx.x;
     const idx_t col0 = tile * (C * G) + grp * C;
     tl.load(cols, col0, n + 1);
     apply_global<TMA>(tl, pp, cols, a, p0, p0, p1, threadIdx.x == 0);
     tl.store(cols, col0, n + 1);
-    if (uflag && (int)blockIdx.x < ucount) {
+    if (uflag) {
         __threadfence();
         __syncthreads();
         if (threadIdx.x == 0) st_release(uflag + tile, utag);
@@ -1632,10 +1662,12 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         if (op.ntiles > 0) {
             if (use_ws)
                 kws<<<(unsigned)op.ntiles, ws_threads, smem_ws, st>>>(
-                    cols, a, d, denoms, m, n, op.p0, op.p1, 0, fail, op.tiles, nullptr, 0, 0);
+                    cols, a, d, denoms, m, n, op.p0, op.p1, 0, fail, op.tiles, nullptr, 0, 0,
+                    nullptr, 0);
             else
                 ku<<<(unsigned)op.ntiles, T * G, smem_u, st>>>(cols, a, d, denoms, m, n, op.p0,
-                                                               op.p1, 0, fail, op.tiles, nullptr, 0, 0);
+                                                               op.p1, 0, fail, op.tiles, nullptr, 0,
+                                                               0, nullptr, 0);
         }
         return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
     }
@@ -1658,10 +1690,12 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         auto update_x = [&](idx_t b) {  // block b -> the x tile (1 CTA)
             if (use_ws)
                 kws<<<1, ws_threads, smem_ws, ss.xs>>>(cols, a, d, denoms, m, n, b * B, blk_end(b),
-                                                       ntiles - 1, fail, nullptr, nullptr, 0, 0);
+                                                       ntiles - 1, fail, nullptr, nullptr, 0, 0,
+                                                       nullptr, 0);
             else
                 ku<<<1, T * G, smem_u, ss.xs>>>(cols, a, d, denoms, m, n, b * B, blk_end(b),
-                                                ntiles - 1, fail, nullptr, nullptr, 0, 0);
+                                                ntiles - 1, fail, nullptr, nullptr, 0, 0, nullptr,
+                                                0);
         };
         cudaEventRecord(ss.e0, st);
         cudaStreamWaitEvent(ss.ps, ss.e0, 0);
@@ -1683,25 +1717,56 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
             cudaStreamWaitEvent(ss.xs, ss.eP, 0);
             update_x(0);
         }
-        auto upd = [&](cudaStream_t s_, idx_t b, idx_t ta, idx_t tb, int* uf, int uc) {
+        // U(b) for b >= 1 is chained to U(b-1) by programmatic dependent
+        // launch: its CTAs may start on the SMs U(b-1)'s last (partial) wave
+        // leaves idle, as soon as every U(b-1) CTA is resident (they signal at
+        // their start).  Ordering then comes from flags, not from the stream:
+        // each CTA waits for panel(b)'s last chunk flag and for its tile's
+        // U(b-1) (tile_done = uflag[tile] >= b, set by every update CTA).
+        const int nch = panel_flag_chunks(CT);
+        auto upd = [&](cudaStream_t s_, idx_t b, idx_t ta, idx_t tb, int* uf) {
             if (ta >= tb) return;
-            if (use_ws)
-                kws<<<(unsigned)(tb - ta), ws_threads, smem_ws, s_>>>(
-                    cols, a, d, denoms, m, n, b * B, blk_end(b), ta, fail, nullptr, uf,
-                    (int)(b + 1), uc);
-            else
-                ku<<<(unsigned)(tb - ta), T * G, smem_u, s_>>>(
-                    cols, a, d, denoms, m, n, b * B, blk_end(b), ta, fail, nullptr, uf,
-                    (int)(b + 1), uc);
+            const bool chained = b > 0;
+            const int* pflag = chained ? flags + (b * B / CT + tiles_of(b) - 1) * nch + nch - 1
+                                       : nullptr;
+            const int need = chained ? (int)b : 0;
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3((unsigned)(tb - ta));
+            lc.stream = s_;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = chained ? 1 : 0;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            const double* dd = d;
+            const double* dn = denoms;
+            const int64_t* no_tiles = nullptr;
+            const int utag = (int)(b + 1);
+            if (use_ws) {
+                lc.blockDim = dim3(ws_threads);
+                lc.dynamicSmemBytes = smem_ws;
+                cudaLaunchKernelEx(&lc, kws, cols, a, dd, dn, m, n, b * B, blk_end(b), ta,
+                                   (const int32_t*)fail, no_tiles, uf, utag, need, pflag, epoch);
+            } else {
+                lc.blockDim = dim3(T * G);
+                lc.dynamicSmemBytes = smem_u;
+                cudaLaunchKernelEx(&lc, ku, cols, a, dd, dn, m, n, b * B, blk_end(b), ta,
+                                   (const int32_t*)fail, no_tiles, uf, utag, need, pflag, epoch);
+            }
         };
         for (idx_t b = 0; b < nb; ++b) {
-            cudaStreamWaitEvent(st, ss.eP, 0);  // panel(b): block b is final
+            // panel(b): block b is final.  U(0) waits for it on the stream; the
+            // chained U(b >= 1) wait inside the kernel (pflag), because a stream
+            // wait between two kernels defeats the programmatic early launch
+            // (tools/micro/pdl_probe2.cu).  No deadlock: panel(b) runs on the
+            // high-priority stream and is resident before U(b) can launch.
+            if (b == 0) cudaStreamWaitEvent(st, ss.eP, 0);
             // eU: the main stream up to U(b-1); panel(b+1) must not be resident
             // (spinning on its SMs) while U(b-1) still runs
             cudaEventRecord(ss.eU, st);
             const idx_t t0 = b + 1 < nb ? (b + 1) * B / CT : (n + CT - 1) / CT;
             prof.mark(st, 0, b, 0);
-            upd(st, b, t0, nt_y, uflag, b + 1 < nb ? (int)tiles_of(b + 1) : 0);
+            upd(st, b, t0, nt_y, uflag);
             prof.mark(st, 0, b, 1);
             if (b + 1 < nb) {
                 const idx_t p0 = (b + 1) * B;
