@@ -1130,7 +1130,7 @@ __global__ void __launch_bounds__(TC + 128, TC == 128 ? 2 : 1)
     }
     tl.store(cols, col0, n + 1);
     if (uflag) {  // tile done: the next panel and the next update may take it
-        __threadfence();
+        // stores -> barrier -> one cumulative gpu-scope release (as the panel)
         named_bar(5, TC);
         if (threadIdx.x == 0) st_release(uflag + col0 / C, utag);
     }
@@ -1162,7 +1162,6 @@ __global__ void __launch_bounds__(T* G, 1)
     apply_global<TMA>(tl, pp, cols, a, p0, p0, p1, threadIdx.x == 0);
     tl.store(cols, col0, n + 1);
     if (uflag) {
-        __threadfence();
         __syncthreads();
         if (threadIdx.x == 0) st_release(uflag + tile, utag);
     }
