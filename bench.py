@@ -363,7 +363,8 @@ def run_ours(args):
         "parallelism": (f"column-sharded cascade over {world} GPUs (dist.py, "
                         f"{args.exchange} block exchange)" if shard
                         else f"replicas x{world}" if world > 1 else "1 GPU"),
-        "cascade_block_pivots": 128 if shard else int(load_lib().pdas_cascade_block_pivots()),
+        "cascade_block_pivots": (int(load_lib().pdas_cascade_block_pivots()) if shard
+                                 else int(load_lib().pdas_cascade_solve_block())),
         "e2e": {"value": jobs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,

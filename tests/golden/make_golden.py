@@ -319,8 +319,36 @@ def gen_breakdown():
     np.savez_compressed(os.path.join(HERE, "breakdown.npz"), **out)
 
 
+def gen_check():
+    """The reference's `adascale check` per seed (cli.py:183-217): the
+    Woodbury and direct solutions, the backend gap and the Z-residual, for the
+    default sweep (seeds 1..20, m and n drawn per seed) and a fixed 20x60 one."""
+    cli = sys.modules["adascale.cli"] if "adascale.cli" in sys.modules else __import__(
+        "adascale.cli", fromlist=["cli"])
+    out = {}
+    for tag, seeds, m, n in (("auto", range(1, 21), None, None), ("m20n60", range(1, 6), 20, 60)):
+        for seed in seeds:
+            rng = np.random.default_rng(seed)
+            mm = m if m is not None else int(rng.integers(1, 6))
+            nn = n if n is not None else int(rng.integers(mm + 1, 9))
+            if mm == 1 and nn == 1:
+                continue
+            a, d, rhs = cli.random_system(rng, mm, nn)
+            z = ad.z_inverse_check(a, d)
+            wd = ad.solve_direct(a, d, rhs)
+            ww = ad.solve_woodbury(ad.prepare_woodbury(a), a, d, rhs)
+            gap = float(np.max(np.abs(ww - wd))) / (1.0 + float(np.max(np.abs(wd))))
+            k = f"{tag}/{seed}"
+            out[k + "/mn"] = np.array([mm, nn])
+            out[k + "/z"], out[k + "/gap"] = np.array(z), np.array(gap)
+            out[k + "/w_direct"], out[k + "/w_woodbury"] = wd, ww
+            out[k + "/A"], out[k + "/d"], out[k + "/rhs"] = a.as_2d(), d, rhs
+    np.savez_compressed(os.path.join(HERE, "check.npz"), **out)
+    print("check.npz", len(out))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["kernels", "c1", "c2"]
     for w in which:
         {"kernels": gen_kernels, "c1": gen_c1, "c2": gen_c2, "c3": gen_c3, "c5": gen_c5,
-         "breakdown": gen_breakdown}[w]()
+         "breakdown": gen_breakdown, "check": gen_check}[w]()

@@ -105,3 +105,15 @@ def test_no_cpu_fallback_without_gpu():
 
 def test_active_core_names_cuda():
     assert P.active_core() == "cuda-sm_100a"
+
+
+def test_harness_argument_parsing():
+    from paper_1502_03543_b200 import harness as H
+
+    assert H.parse_seed_range("1..4") == [1, 2, 3, 4] and H.parse_seed_range("7") == [7]
+    for bad in ("4..1", "a..b", "x"):
+        with pytest.raises(ValueError):
+            H.parse_seed_range(bad)
+    assert H.parse_grid("50x200,2000X20000") == [(50, 200), (2000, 20000)]
+    with pytest.raises(ValueError):
+        H.parse_grid("50by200")
