@@ -1624,14 +1624,19 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
     // The panel's pivot data always comes through the TMA ring when it can
     // (prefetched S stages ahead, also where the update loads straight from
     // L2): a latency chain cannot hide an L2 round trip per step.
-    constexpr int SP = TMA ? S : 4;
-    const bool ptma = (TMA || TP >= 128) && m % 2 == 0 &&
-                      ((uintptr_t)cols | (uintptr_t)a) % 16 == 0 &&
-                      casc_smem_bytes<TP, CT, 1>(SP, m) <= 200 * 1024;
-    const size_t smem_p = casc_smem_bytes<TP, CT, 1>(ptma ? SP : 0, m);
+    // 4 stages when they fit next to the panel's reduction rows, else 2, else
+    // direct loads (m beyond ~6000)
+    const bool pok = (TMA || TP >= 128) && !GEN && m % 2 == 0 &&
+                     ((uintptr_t)cols | (uintptr_t)a) % 16 == 0;
+    constexpr size_t kPanelSmem = 200 * 1024;
+    const int sp = pok && casc_smem_bytes<TP, CT, 1>(4, m) <= kPanelSmem   ? 4
+                   : pok && casc_smem_bytes<TP, CT, 1>(2, m) <= kPanelSmem ? 2
+                                                                           : 0;
+    const size_t smem_p = casc_smem_bytes<TP, CT, 1>(sp, m);
     auto ku = k_casc_update<TMA, S, T, R, Cu, G, GEN>;
-    auto kp = ptma ? k_casc_panel<!GEN, SP, TP, RP, CT, GEN>
-                   : k_casc_panel<false, SP, TP, RP, CT, GEN>;
+    auto kp = sp == 4   ? k_casc_panel<!GEN, 4, TP, RP, CT, GEN>
+              : sp == 2 ? k_casc_panel<!GEN, 2, TP, RP, CT, GEN>
+                        : k_casc_panel<false, 1, TP, RP, CT, GEN>;
     cudaFuncSetAttribute(ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_u);
     cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
     // warp-specialized update for the 256-thread single-group layouts
