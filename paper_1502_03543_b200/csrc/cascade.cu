@@ -1475,6 +1475,160 @@ __global__ void k_peer_wait(const int* __restrict__ flags, idx_t t0, idx_t t1, i
     }
 }
 
+// ------------------------------------------------------------ small cascade
+// m <= 64 (H <= 32) with [Y | x] and A both resident in one SM's shared
+// memory (c1: 80 KB + 80 KB): the whole cascade in ONE CTA, step by step,
+// no panels, no flags, no global memory between steps.  A column's tree
+// lives in a group of LPC lanes: lane j of the group owns s-indices
+// j + LPC r (r < RPL = H / LPC), i.e. rows j + LPC r and j + LPC r + H, so the
+// levels h >= LPC are in-lane register adds and the last log2(LPC) are xor
+// shuffles inside the group -- a warp reduces 32 / LPC columns with the same
+// shuffles.  Step l: warp 0 finds denom_l from the pivot column while every
+// group reduces its columns k > l; barrier; each group divides (all of its
+// lanes: same bits) and updates its column; barrier (column l+1 is final).
+// Computing inner_k then updating column k per column equals the reference's
+// phase 1 / phase 2 split (_kernels.pyx:247-266): the pivot column is not
+// written in step l.
+constexpr int kSmallThreads = 256;
+constexpr int KB = 1;  // columns per group and pass (k_casc_small; 2 measured no better)
+
+__host__ __device__ inline size_t small_cascade_smem(idx_t m, idx_t n) {
+    return (size_t)((n + 1) * m + n * m + n) * sizeof(double);
+}
+
+template <int LPC, int RPL>
+__global__ void __launch_bounds__(kSmallThreads, 1)
+    k_casc_small(double* __restrict__ cols, const double* __restrict__ a,
+                 const double* __restrict__ d, int m, int n, int32_t* __restrict__ fail) {
+    extern __shared__ __align__(16) double smx[];
+    double* sc = smx;                          // [n + 1][m]
+    double* sa = smx + (size_t)(n + 1) * m;    // [n][m]
+    double* sdv = sa + (size_t)n * m;          // d
+    const int tid = threadIdx.x;
+    constexpr int NG = kSmallThreads / LPC;    // column groups per CTA
+    const int grp = tid / LPC, j = tid % LPC;
+    for (idx_t i = tid; i < (idx_t)(n + 1) * m; i += kSmallThreads) sc[i] = __ldcg(cols + i);
+    for (idx_t i = tid; i < (idx_t)n * m; i += kSmallThreads) sa[i] = __ldg(a + i);
+    for (int i = tid; i < n; i += kSmallThreads) sdv[i] = __ldg(d + i);
+    __syncthreads();
+    const bool m1 = m == 1;
+    const int H = m > 1 ? (int)(pow2_ceil(m) >> 1) : 0;
+    // rows of this lane: lo = j + LPC r, hi = lo + H (absent rows: +0.0 terms)
+    bool lo_ok[RPL], hi_ok[RPL];
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+        const int lo = j + LPC * r;
+        lo_ok[r] = m1 ? lo == 0 : lo < H;
+        hi_ok[r] = !m1 && lo < H && lo + H < m;
+    }
+    // tree over a column (its values left in xl/xh for the update): level 0 per
+    // s-index (+0.0 pad, _kernels.pyx:46), in-lane levels, then the group's xor
+    // butterfly; every lane of the group ends with the result
+    auto tree = [&](const double (&vl)[RPL], const double (&vh)[RPL], const double* col,
+                    double (&xl)[RPL], double (&xh)[RPL]) {
+        double q[RPL];
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+            xl[r] = lo_ok[r] ? col[j + LPC * r] : 0.0;
+            xh[r] = hi_ok[r] ? col[j + LPC * r + H] : 0.0;
+            const double lo = lo_ok[r] ? vl[r] * xl[r] : 0.0;
+            const double hi = hi_ok[r] ? vh[r] * xh[r] : 0.0;
+            q[r] = m1 ? lo : lo + hi;
+        }
+        double t = lane_tree<RPL>(q);
+#pragma unroll
+        for (int sft = LPC / 2; sft >= 1; sft >>= 1) t = t + __shfl_xor_sync(0xffffffffu, t, sft);
+        return t;
+    };
+    int32_t f = 0;
+    for (int l = 0; l < n; ++l) {
+        const double dl = sdv[l];
+        if (dl == 1.0) continue;  // _kernels.pyx:242-243 (uniform)
+        const double fl = dl - 1.0;
+        const double* al = sa + (size_t)l * m;
+        const double* pl = sc + (size_t)l * m;
+        double vl[RPL], vh[RPL], pv_lo[RPL], pv_hi[RPL];
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+            const int lo = j + LPC * r;
+            vl[r] = lo_ok[r] ? al[lo] * fl : 0.0;
+            vh[r] = hi_ok[r] ? al[lo + H] * fl : 0.0;
+        }
+        // every warp finds denom_l itself (same bits everywhere: no barrier)
+        const double inner_l = tree(vl, vh, pl, pv_lo, pv_hi);
+        const double denom = 1.0 + inner_l;
+        if (fabs(denom) <= kDenomEpsRel * (1.0 + fabs(inner_l))) {
+            f = l + 1;  // the same test in every thread: uniform exit
+            break;
+        }
+        // this group's columns past l: k0, k0 + NG, ...; shuffles stay
+        // warp-uniform (a group past n reduces the pivot column and drops it)
+        const int k0 = l + 1 + ((grp - (l + 1)) % NG + NG) % NG;
+        // KB columns per pass, their chains (loads, tree, divide, update) overlapped
+        for (int kb = k0; __any_sync(0xffffffffu, kb <= n); kb += KB * NG) {
+            double xl[KB][RPL], xh[KB][RPL], g[KB];
+#pragma unroll
+            for (int b = 0; b < KB; ++b) {
+                const int k = kb + b * NG;
+                const double* ck = sc + (size_t)(k <= n ? k : l) * m;
+                g[b] = tree(vl, vh, ck, xl[b], xh[b]);
+            }
+#pragma unroll
+            for (int b = 0; b < KB; ++b) g[b] = g[b] / denom;
+#pragma unroll
+            for (int b = 0; b < KB; ++b) {
+                const int k = kb + b * NG;
+                if (k > n) continue;
+                double* ck = sc + (size_t)k * m;
+#pragma unroll
+                for (int r = 0; r < RPL; ++r) {
+                    const int lo = j + LPC * r;
+                    if (lo_ok[r]) {
+                        const double q = g[b] * pv_lo[r];
+                        ck[lo] = xl[b][r] - q;
+                    }
+                    if (hi_ok[r]) {
+                        const double q = g[b] * pv_hi[r];
+                        ck[lo + H] = xh[b][r] - q;
+                    }
+                }
+            }
+        }
+        __syncthreads();  // column l+1 is final for the next step
+    }
+    if (f) {
+        if (tid == 0) *fail = f;
+        return;  // on breakdown only the return code is contractual
+    }
+    for (idx_t i = tid; i < (idx_t)(n + 1) * m; i += kSmallThreads) cols[i] = sc[i];
+}
+
+static bool small_cascade_fits(idx_t m, idx_t n) {
+    return m >= 1 && m <= 64 && n >= 1 && small_cascade_smem(m, n) <= 200 * 1024;
+}
+
+template <int LPC, int RPL>
+static int launch_small(double* cols, const double* a, const double* d, idx_t m, idx_t n,
+                        int32_t* fail, cudaStream_t st) {
+    const size_t smem = small_cascade_smem(m, n);
+    cudaFuncSetAttribute(k_casc_small<LPC, RPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    k_casc_small<LPC, RPL><<<1, kSmallThreads, smem, st>>>(cols, a, d, (int)m, (int)n, fail);
+    return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
+}
+
+// groups of 8 lanes per column (up to 4 s-indices each); fewer for H < 8
+static int launch_small_cascade(double* cols, const double* a, const double* d, idx_t m, idx_t n,
+                                int32_t* fail, cudaStream_t st) {
+    const idx_t H = m > 1 ? pow2_ceil(m) >> 1 : 0;
+    if (H == 32) return launch_small<8, 4>(cols, a, d, m, n, fail, st);
+    if (H == 16) return launch_small<8, 2>(cols, a, d, m, n, fail, st);
+    if (H == 8) return launch_small<8, 1>(cols, a, d, m, n, fail, st);
+    if (H == 4) return launch_small<4, 1>(cols, a, d, m, n, fail, st);
+    if (H == 2) return launch_small<2, 1>(cols, a, d, m, n, fail, st);
+    return launch_small<1, 1>(cols, a, d, m, n, fail, st);  // m <= 2
+}
+
 // ------------------------------------------------------------ host side
 struct CascCfg {
     int T, R, Cu, G, CT;
@@ -1895,6 +2049,7 @@ int launch_cascade(double* cols, const double* a, const double* d, idx_t m, idx_
     if (m < 1 || n < 0 || m > INT_MAX / 4) return PDAS_ERR_ARG;
     cudaMemsetAsync(fail_dev, 0, sizeof(int32_t), st);
     if (n == 0) return PDAS_OK;
+    if (small_cascade_fits(m, n)) return launch_small_cascade(cols, a, d, m, n, fail_dev, st);
     const int B = block_pivots > 0 ? block_pivots : kSolveBlock;
     return dispatch_cascade(cols, a, d, m, n, denoms, fail_dev, flags, epoch, B, st, CascOp{});
 }
@@ -1905,6 +2060,10 @@ int launch_cascade_x0(double* cols, const double* a, const double* d, const doub
     if (m < 1 || n < 0 || m > INT_MAX / 4) return PDAS_ERR_ARG;
     cudaMemsetAsync(fail_dev, 0, sizeof(int32_t), st);
     if (n == 0) return launch_solve_one(low, m, cols, work, st);
+    if (small_cascade_fits(m, n)) {  // x0 first, then the one-CTA cascade
+        const int rc = launch_solve_one(low, m, cols + (size_t)n * m, work, st);
+        return rc ? rc : launch_small_cascade(cols, a, d, m, n, fail_dev, st);
+    }
     CascOp op;
     op.x0_low = low;
     op.x0_work = work;

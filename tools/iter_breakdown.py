@@ -1,4 +1,6 @@
-"""CUDA-event breakdown of one PDAS iteration on the c3 workload."""
+"""CUDA-event breakdown of one PDAS iteration (default c3; --m/--n for others).
+
+    python tools/iter_breakdown.py [--m 50 --n 200]"""
 import os
 import sys
 import time
@@ -11,7 +13,13 @@ from paper_1502_03543_b200 import _device as dv  # noqa: E402
 from paper_1502_03543_b200._lib import OFF_CASCADE_FAIL, call  # noqa: E402
 from paper_1502_03543_b200.engine import DeviceProblem, DeviceSolver, d_mat_vec, d_solve_many  # noqa: E402
 
-m, n = 2000, 20000
+import argparse
+
+ap = argparse.ArgumentParser()
+ap.add_argument('--m', type=int, default=2000)
+ap.add_argument('--n', type=int, default=20000)
+args = ap.parse_args()
+m, n = args.m, args.n
 lp, start = P.gen_random_feasible(m, n, 0)
 prob = DeviceProblem.from_lp(lp)
 eng = DeviceSolver(prob, L0=prob.validate())
