@@ -41,7 +41,9 @@ gloo in the CPU tests); `run_lockstep` drives G in-process virtual ranks in
 lock-step (the broadcast becomes a copy), which is how one GPU checks the
 sharded path without running ranks that wait on each other.
 
-Fused exchange (exchange="peer"): instead of broadcasting a
+Fused exchange (exchange="peer"; EXPERIMENTAL until it has run
+on two real GPUs -- so far only virtual ranks on one device and a 1-rank
+group have exercised it): instead of broadcasting a
 block after its panel, the owner's panel kernel stores each finished tile
 from registers straight into every peer's [Y | x] (and denominators, fail
 word) through NVLink peer mappings and releases a per-tile flag there

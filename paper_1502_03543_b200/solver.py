@@ -293,8 +293,9 @@ def solve_lp(
     calling with the same problem): the Woodbury cascade then runs
     column-sharded over the group (dist.py); results are bitwise the 1-GPU
     ones on every rank.  exchange: "nccl" (one broadcast per pivot block) or
-    "peer" (the panel stores finished blocks straight into the peers' buffers
-    over NVLink, torch symmetric memory; dist.ShardedSolver).
+    "peer" (EXPERIMENTAL: the panel stores finished blocks straight into the
+    peers' buffers over NVLink, torch symmetric memory; dist.ShardedSolver --
+    not yet run on two real GPUs).
     """
     opts = opts or SolveOptions()
     prob = DeviceProblem.from_lp(lp)
