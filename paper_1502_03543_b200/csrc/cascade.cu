@@ -1181,7 +1181,7 @@ __device__ __forceinline__ bool panel_triangle(Tile<T, R, C, GEN>& tl, Pipe<S>& 
                                                double* bc, bool producer,
                                                double* __restrict__ cols = nullptr, idx_t n = 0,
                                                int* __restrict__ cflags = nullptr, int epoch = 0,
-                                               bool trace = false) {
+                                               bool trace = false, int* s_pub = nullptr) {
     (void)trace;
 #if PDAS_HOP_TRACE
     long long tq = clock64();
@@ -1280,11 +1280,17 @@ __device__ __forceinline__ bool panel_triangle(Tile<T, R, C, GEN>& tl, Pipe<S>& 
             // end of a chunk: its columns are final -- store and publish them so
             // the next tile's CTA starts on them while this triangle goes on
             constexpr int CH = C / kPanelChunks > 0 ? C / kPanelChunks : 1;
-            if (cflags && (cl + 1) % CH == 0 && cl + 1 < C && cl + 1 < cnt && !broken) {
+            if (s_pub && cflags && (cl + 1) % CH == 0 && cl + 1 < C && cl + 1 < cnt) {
+                // publisher warp: the compute threads store and arrive (no wait);
+                // the publisher warp's barrier.sync orders their stores before its
+                // cumulative release, so no compute thread ever waits on a fence
+                if (!broken) tl.store(cols, col0, n + 1, cl + 1 - CH, cl + 1);
+                if (producer) *s_pub = broken ? 0 : 1;
+                named_arrive(2, T + 32);
+            } else if (cflags && (cl + 1) % CH == 0 && cl + 1 < C && cl + 1 < cnt && !broken) {
                 // stores -> CTA barrier -> one gpu-scope release by the producer:
                 // the barrier orders every thread's stores before the release,
-                // which is cumulative (the cooperative-groups grid-sync pattern),
-                // so the compute threads never wait on a fence themselves
+                // which is cumulative (the cooperative-groups grid-sync pattern)
                 tl.store(cols, col0, n + 1, cl + 1 - CH, cl + 1);
                 tl.sync();
                 if (producer) st_release(cflags + (cl + 1) / CH - 1, epoch);
@@ -1304,8 +1310,11 @@ __device__ __forceinline__ bool panel_triangle(Tile<T, R, C, GEN>& tl, Pipe<S>& 
 // then the pivots of this block's earlier tiles as their CTAs publish them
 // (flags[tile] == epoch), then the in-register triangle; publish.  Breakdown
 // is detected here, in step order, and reported as the 1-based step.
-template <bool TMA, int S, int T, int R, int C, bool GEN>
-__global__ void __launch_bounds__(T, 1)
+// PW = 32: one extra publisher warp that issues the mid-triangle chunk
+// releases (fence + flag) so the compute threads never stall on them
+// (~3.7 us per publication at c2, profiles/r02_hop_trace.txt).
+template <bool TMA, int S, int T, int R, int C, bool GEN, int PW = 0>
+__global__ void __launch_bounds__(T + PW, 1)
     k_casc_panel(double* __restrict__ cols, const double* __restrict__ a,
                  const double* __restrict__ d, double* __restrict__ denoms, int m, idx_t n,
                  idx_t q0, idx_t p0, idx_t p1, int32_t* __restrict__ fail, int* __restrict__ flags,
@@ -1330,8 +1339,10 @@ __global__ void __launch_bounds__(T, 1)
     stage_scalars(pp, d, denoms, q0, q0, p0, true);
     for (idx_t l = p0 + threadIdx.x; l < p1; l += blockDim.x) pp.sd[l - q0] = __ldg(d + l);
     __syncthreads();
+    const bool pubw = PW > 0 && (int)threadIdx.x >= T;  // the publisher warp
+    __shared__ int s_pub;
     Tile<T, R, C, GEN> tl;
-    tl.init(threadIdx.x, m, 1, red, bc);
+    tl.init(pubw ? 0 : (int)threadIdx.x, m, 1, red, bc);
     const bool producer = threadIdx.x == 0;
     const idx_t col0 = tile * C;
     bool dead = false;
@@ -1349,7 +1360,7 @@ __global__ void __launch_bounds__(T, 1)
             }
         dead = __syncthreads_or(producer && *(volatile int32_t*)fail != 0);
     }
-    if (!dead) {
+    if (!dead && !pubw) {
         tl.load(cols, col0, n + 1);
         apply_global<TMA>(tl, pp, cols, a, q0, q0, p0, producer);
     }
@@ -1407,17 +1418,31 @@ __global__ void __launch_bounds__(T, 1)
             }
             __syncthreads();
             HOP_MARK(hop_here, 4);
-            apply_global<TMA>(tl, pp, cols, a, q0, pa, pb, producer, true);
+            if (!pubw) apply_global<TMA>(tl, pp, cols, a, q0, pa, pb, producer, true);
             HOP_MARK(hop_here, 5);
             PANEL_LAP(t_apply);
         }
     }
     bool stored = false;
     HOP_MARK(hop_con, 6);
-    if (!dead) {
+    if (!dead && pubw) {
+        // the publisher warp: one barrier per mid-triangle publication point
+        int* cf = NCH > 1 ? flags + tile * NCH : nullptr;
+        const int cnt = (int)((col0 + C < p1 ? col0 + C : p1) - col0);
+        constexpr int CHP = C / kPanelChunks > 0 ? C / kPanelChunks : 1;
+        for (int cl = 0; cl < C; ++cl) {
+            if (cl < cnt && cf && (cl + 1) % CHP == 0 && cl + 1 < C && cl + 1 < cnt) {
+                named_bar(2, T + 32);
+                if ((threadIdx.x & 31) == 0 && s_pub) {
+                    __threadfence();
+                    st_relaxed(cf + (cl + 1) / CHP - 1, epoch);
+                }
+            }
+        }
+    } else if (!dead) {
         const bool broken = panel_triangle<TMA, S, T, R, C, GEN>(
             tl, pp, a, denoms, m, col0, p1, q0, fail, bc, producer, cols, n,
-            NCH > 1 ? flags + tile * NCH : nullptr, epoch, hop_con);
+            NCH > 1 ? flags + tile * NCH : nullptr, epoch, hop_con, PW > 0 ? &s_pub : nullptr);
         HOP_MARK(hop_pub, 0);
         if (!broken) {
             tl.store(cols, col0, n + 1);
@@ -1441,7 +1466,7 @@ __global__ void __launch_bounds__(T, 1)
         // multi-GPU exchange fused into the panel: the tile's final columns go
         // from registers straight into every peer's [Y|x] over NVLink, with
         // their denominators; then one system-scope flag per peer and tile
-        if (stored) {
+        if (stored && !pubw) {
             for (int q = 0; q < peers.count; ++q) tl.store(peers.cols[q], col0, n + 1);
             if (threadIdx.x < C && col0 + threadIdx.x < p1) {
                 const double den = __ldcg(denoms + col0 + threadIdx.x);
@@ -1788,9 +1813,12 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
                                                                            : 0;
     const size_t smem_p = casc_smem_bytes<TP, CT, 1>(sp, m);
     auto ku = k_casc_update<TMA, S, T, R, Cu, G, GEN>;
-    auto kp = sp == 4   ? k_casc_panel<!GEN, 4, TP, RP, CT, GEN>
-              : sp == 2 ? k_casc_panel<!GEN, 2, TP, RP, CT, GEN>
-                        : k_casc_panel<false, 1, TP, RP, CT, GEN>;
+    // a publisher warp where the registers allow it (TP <= 256: c2, c4, c5)
+    constexpr int PW = (TP <= 256 && !GEN) ? 32 : 0;
+    constexpr int TPB = TP + PW;  // panel block size
+    auto kp = sp == 4   ? k_casc_panel<!GEN, 4, TP, RP, CT, GEN, PW>
+              : sp == 2 ? k_casc_panel<!GEN, 2, TP, RP, CT, GEN, PW>
+                        : k_casc_panel<false, 1, TP, RP, CT, GEN, PW>;
     cudaFuncSetAttribute(ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_u);
     cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
     // warp-specialized update for the 256-thread single-group layouts
@@ -1811,7 +1839,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
     const idx_t ntiles = (n + 1 + CT - 1) / CT;
     if (op.kind == 1) {
         if (op.p0 % CT || op.p1 <= op.p0 || op.p1 - op.q0 > 2 * kMaxBlock) return PDAS_ERR_ARG;
-        kp<<<(unsigned)((op.p1 - op.p0 + CT - 1) / CT), TP, smem_p, st>>>(
+        kp<<<(unsigned)((op.p1 - op.p0 + CT - 1) / CT), TPB, smem_p, st>>>(
             cols, a, d, denoms, m, n, op.q0, op.p0, op.p1, fail, flags, epoch, nullptr, 0, op.peers);
         return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
     }
@@ -1866,7 +1894,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
             }
         }
         prof.mark(ss.ps, 1, 0, 0);
-        kp<<<(unsigned)tiles_of(0), TP, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, 0, 0,
+        kp<<<(unsigned)tiles_of(0), TPB, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, 0, 0,
                                                         blk_end(0), fail, flags, epoch, nullptr, 0,
                                                         PeerSet{});
         prof.mark(ss.ps, 1, 0, 1);
@@ -1930,7 +1958,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
                 const idx_t p0 = (b + 1) * B;
                 cudaStreamWaitEvent(ss.ps, ss.eU, 0);
                 prof.mark(ss.ps, 1, b + 1, 0);
-                kp<<<(unsigned)tiles_of(b + 1), TP, smem_p, ss.ps>>>(
+                kp<<<(unsigned)tiles_of(b + 1), TPB, smem_p, ss.ps>>>(
                     cols, a, d, denoms, m, n, p0, p0, blk_end(b + 1), fail, flags, epoch, uflag,
                     (int)(b + 1), PeerSet{});
                 prof.mark(ss.ps, 1, b + 1, 1);
