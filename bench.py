@@ -210,9 +210,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PDAS_BENCH_BACKEND=gloo runs the N > 1 code path with several ranks on one
+    # GPU (a functional check of the sharded bench; timings are meaningless)
+    backend = os.environ.get("PDAS_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     import paper_1502_03543_b200 as P
     from paper_1502_03543_b200 import _device as dv
