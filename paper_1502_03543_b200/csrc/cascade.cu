@@ -1515,10 +1515,15 @@ __global__ void k_peer_wait(const int* __restrict__ flags, idx_t t0, idx_t t1, i
 // phase 1 / phase 2 split (_kernels.pyx:247-266): the pivot column is not
 // written in step l.
 constexpr int kSmallThreads = 256;
-constexpr int KB = 1;  // columns per group and pass (k_casc_small; 2 measured no better)
+constexpr int KB = 1;  // columns per group and pass (k_casc_small; 2 and 4 measured slower)
+
+// shared-memory column stride: m rounded up to 8 (mod 16) doubles, so the four
+// 8-lane groups of a warp (consecutive columns) fall into two bank halves
+__host__ __device__ inline idx_t small_stride(idx_t m) { return (m + 7) / 16 * 16 + 8; }
 
 __host__ __device__ inline size_t small_cascade_smem(idx_t m, idx_t n) {
-    return (size_t)((n + 1) * m + n * m + n) * sizeof(double);
+    const idx_t mp = small_stride(m);
+    return (size_t)((n + 1) * mp + n * mp + n) * sizeof(double);
 }
 
 template <int LPC, int RPL>
@@ -1526,14 +1531,16 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     k_casc_small(double* __restrict__ cols, const double* __restrict__ a,
                  const double* __restrict__ d, int m, int n, int32_t* __restrict__ fail) {
     extern __shared__ __align__(16) double smx[];
-    double* sc = smx;                          // [n + 1][m]
-    double* sa = smx + (size_t)(n + 1) * m;    // [n][m]
-    double* sdv = sa + (size_t)n * m;          // d
+    const int mp = (int)small_stride(m);
+    double* sc = smx;                          // [n + 1][mp]
+    double* sa = smx + (size_t)(n + 1) * mp;   // [n][mp]
+    double* sdv = sa + (size_t)n * mp;         // d
     const int tid = threadIdx.x;
     constexpr int NG = kSmallThreads / LPC;    // column groups per CTA
     const int grp = tid / LPC, j = tid % LPC;
-    for (idx_t i = tid; i < (idx_t)(n + 1) * m; i += kSmallThreads) sc[i] = __ldcg(cols + i);
-    for (idx_t i = tid; i < (idx_t)n * m; i += kSmallThreads) sa[i] = __ldg(a + i);
+    for (idx_t e = tid; e < (idx_t)(n + 1) * m; e += kSmallThreads)
+        sc[(e / m) * mp + e % m] = __ldcg(cols + e);
+    for (idx_t e = tid; e < (idx_t)n * m; e += kSmallThreads) sa[(e / m) * mp + e % m] = __ldg(a + e);
     for (int i = tid; i < n; i += kSmallThreads) sdv[i] = __ldg(d + i);
     __syncthreads();
     const bool m1 = m == 1;
@@ -1570,8 +1577,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
         const double dl = sdv[l];
         if (dl == 1.0) continue;  // _kernels.pyx:242-243 (uniform)
         const double fl = dl - 1.0;
-        const double* al = sa + (size_t)l * m;
-        const double* pl = sc + (size_t)l * m;
+        const double* al = sa + (size_t)l * mp;
+        const double* pl = sc + (size_t)l * mp;
         double vl[RPL], vh[RPL], pv_lo[RPL], pv_hi[RPL];
 #pragma unroll
         for (int r = 0; r < RPL; ++r) {
@@ -1595,7 +1602,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
 #pragma unroll
             for (int b = 0; b < KB; ++b) {
                 const int k = kb + b * NG;
-                const double* ck = sc + (size_t)(k <= n ? k : l) * m;
+                const double* ck = sc + (size_t)(k <= n ? k : l) * mp;
                 g[b] = tree(vl, vh, ck, xl[b], xh[b]);
             }
 #pragma unroll
@@ -1604,7 +1611,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
             for (int b = 0; b < KB; ++b) {
                 const int k = kb + b * NG;
                 if (k > n) continue;
-                double* ck = sc + (size_t)k * m;
+                double* ck = sc + (size_t)k * mp;
 #pragma unroll
                 for (int r = 0; r < RPL; ++r) {
                     const int lo = j + LPC * r;
@@ -1625,7 +1632,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
         if (tid == 0) *fail = f;
         return;  // on breakdown only the return code is contractual
     }
-    for (idx_t i = tid; i < (idx_t)(n + 1) * m; i += kSmallThreads) cols[i] = sc[i];
+    for (idx_t e = tid; e < (idx_t)(n + 1) * m; e += kSmallThreads) cols[e] = sc[(e / m) * mp + e % m];
 }
 
 static bool small_cascade_fits(idx_t m, idx_t n) {
