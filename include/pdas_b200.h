@@ -145,6 +145,20 @@ int pdas_solve_sweeps_ws_x0(double* cols, const double* a, const double* d, cons
  * p1).  No-op when *fail_dev != 0.  ws/epoch follow pdas_solve_sweeps_ws. */
 int pdas_cascade_tile_width(int64_t m);
 int pdas_cascade_block_pivots(void);
+/* The chained (early-panel) form of the two blocks, as on one GPU: an update
+ * that also publishes tile_done[t] = utag for every tile it updates, and a
+ * panel over block [p0, p1) that applies no previous block itself but waits
+ * in-kernel until each of its tiles reports tile_done == utag (the rank's own
+ * update of the previous block).  utag = b + 1 for block b's update; the
+ * tags are zeroed per cascade with pdas_cascade_reset_tags.  dist.py. */
+int pdas_cascade_panel_chained(double* cols, const double* a, const double* d, int64_t m,
+                               int64_t n, int64_t p0, int64_t p1, void* ws, int32_t epoch,
+                               int32_t* fail_dev, int32_t utag, void* stream);
+int pdas_cascade_update_tagged(double* cols, const double* a, const double* d, int64_t m,
+                               int64_t n, int64_t p0, int64_t p1, const int64_t* tiles_dev,
+                               int64_t ntiles, void* ws, int32_t* fail_dev, int32_t utag,
+                               void* stream);
+int pdas_cascade_reset_tags(void* ws, int64_t n, void* stream);
 /* Pivots per block of the 1-GPU cascade (pdas_solve_sweeps_ws / _x0). */
 int pdas_cascade_solve_block(void);
 int pdas_cascade_panel(double* cols, const double* a, const double* d, int64_t m, int64_t n,

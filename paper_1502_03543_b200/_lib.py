@@ -84,6 +84,11 @@ SIGNATURES = {
     "pdas_cascade_panel_peers": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, _I64, _I64, _I64, _VP,
                                                 ctypes.c_int32, _VP, ctypes.c_int32, _VP, _VP, _VP,
                                                 _VP]),
+    "pdas_cascade_panel_chained": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, _I64, _I64, _VP,
+                                                  ctypes.c_int32, _VP, ctypes.c_int32, _VP]),
+    "pdas_cascade_update_tagged": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, _I64, _I64, _VP, _I64,
+                                                  _VP, _VP, ctypes.c_int32, _VP]),
+    "pdas_cascade_reset_tags": (ctypes.c_int, [_VP, _I64, _VP]),
     "pdas_cascade_peer_wait": (ctypes.c_int, [_VP, _I64, _I64, _I64, _I64, ctypes.c_int32, _VP]),
     "pdas_cholesky_solve_one": (ctypes.c_int, [_VP, _I64, _VP, _VP]),
     "pdas_iter_reset": (ctypes.c_int, [_VP, _VP]),

@@ -316,6 +316,57 @@ int pdas_cascade_update(double* cols, const double* a, const double* d, int64_t 
                       "cascade_update");
 }
 
+int pdas_cascade_panel_chained(double* cols, const double* a, const double* d, int64_t m,
+                               int64_t n, int64_t p0, int64_t p1, void* ws, int32_t epoch,
+                               int32_t* fail_dev, int32_t utag, void* stream) {
+    if (m < 1 || n < 1 || fail_dev == nullptr || ws == nullptr || epoch < 1 || utag < 0)
+        return set_err(PDAS_ERR_ARG, "cascade_panel_chained: bad args");
+    if (m > pdas::cascade_supported_m())
+        return set_err(PDAS_ERR_UNSUPPORTED,
+                       "cascade_panel_chained: m above the compiled configurations");
+    const int ct = pdas::cascade_tile_width(m);
+    if (p0 < 0 || p0 >= p1 || p1 > n || p0 % ct != 0 || p1 - p0 > pdas::kShardBlock)
+        return set_err(PDAS_ERR_ARG, "cascade_panel_chained: block bounds");
+    double* denoms;
+    int* flags;
+    split_ws(ws, n, &denoms, &flags);
+    return check_cuda(pdas::launch_cascade_panel(cols, a, d, m, n, p0, p0, p1, denoms, fail_dev,
+                                                 flags, epoch, S(stream), nullptr, utag),
+                      "cascade_panel_chained");
+}
+
+int pdas_cascade_update_tagged(double* cols, const double* a, const double* d, int64_t m,
+                               int64_t n, int64_t p0, int64_t p1, const int64_t* tiles_dev,
+                               int64_t ntiles, void* ws, int32_t* fail_dev, int32_t utag,
+                               void* stream) {
+    if (m < 1 || n < 1 || fail_dev == nullptr || ws == nullptr || ntiles < 0 || utag < 1 ||
+        (ntiles > 0 && tiles_dev == nullptr))
+        return set_err(PDAS_ERR_ARG, "cascade_update_tagged: bad args");
+    if (m > pdas::cascade_supported_m())
+        return set_err(PDAS_ERR_UNSUPPORTED,
+                       "cascade_update_tagged: m above the compiled configurations");
+    if (p0 < 0 || p0 >= p1 || p1 > n || p1 - p0 > pdas::kShardBlock)
+        return set_err(PDAS_ERR_ARG, "cascade_update_tagged: block bounds");
+    double* denoms;
+    int* flags;
+    split_ws(ws, n, &denoms, &flags);
+    return check_cuda(pdas::launch_cascade_update(cols, a, d, m, n, p0, p1, tiles_dev, ntiles,
+                                                  denoms, fail_dev, S(stream), flags, utag),
+                      "cascade_update_tagged");
+}
+
+int pdas_cascade_reset_tags(void* ws, int64_t n, void* stream) {
+    if (ws == nullptr || n < 1) return set_err(PDAS_ERR_ARG, "cascade_reset_tags: bad args");
+    double* denoms;
+    int* flags;
+    split_ws(ws, n, &denoms, &flags);
+    return check_cuda(
+        cudaMemsetAsync(flags + (n + 2), 0, sizeof(int) * (size_t)(n + 2), S(stream)) == cudaSuccess
+            ? PDAS_OK
+            : PDAS_ERR_CUDA,
+        "cascade_reset_tags");
+}
+
 int pdas_cholesky_solve_one(const double* low, int64_t m, double* x, void* stream) {
     if (m < 1) return set_err(PDAS_ERR_ARG, "cholesky_solve_one: bad shape");
     double* work = nullptr;

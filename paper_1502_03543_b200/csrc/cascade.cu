@@ -1788,6 +1788,10 @@ struct CascOp {
     const double* x0_low = nullptr;
     double* x0_work = nullptr;
     PeerSet peers{};  // kind 1 only: fused multi-GPU exchange
+    // kinds 1 / 2 of the chained sharded schedule: a panel waits for its tiles'
+    // tile_done == utag (kind 1, q0 == p0); an update publishes tile_done = utag
+    int* uflag = nullptr;
+    int utag = 0;
 };
 
 // The panel is a latency chain (one full-tile reduction per pivot step on one
@@ -1847,7 +1851,8 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
     if (op.kind == 1) {
         if (op.p0 % CT || op.p1 <= op.p0 || op.p1 - op.q0 > 2 * kMaxBlock) return PDAS_ERR_ARG;
         kp<<<(unsigned)((op.p1 - op.p0 + CT - 1) / CT), TPB, smem_p, st>>>(
-            cols, a, d, denoms, m, n, op.q0, op.p0, op.p1, fail, flags, epoch, nullptr, 0, op.peers);
+            cols, a, d, denoms, m, n, op.q0, op.p0, op.p1, fail, flags, epoch, op.uflag, op.utag,
+            op.peers);
         return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
     }
     if (op.kind == 2) {
@@ -1855,12 +1860,12 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         if (op.ntiles > 0) {
             if (use_ws)
                 kws<<<(unsigned)op.ntiles, ws_threads, smem_ws, st>>>(
-                    cols, a, d, denoms, m, n, op.p0, op.p1, 0, fail, op.tiles, nullptr, 0, 0,
-                    nullptr, 0);
+                    cols, a, d, denoms, m, n, op.p0, op.p1, 0, fail, op.tiles, op.uflag, op.utag,
+                    0, nullptr, 0);
             else
                 ku<<<(unsigned)op.ntiles, T * G, smem_u, st>>>(cols, a, d, denoms, m, n, op.p0,
-                                                               op.p1, 0, fail, op.tiles, nullptr, 0,
-                                                               0, nullptr, 0);
+                                                               op.p1, 0, fail, op.tiles, op.uflag,
+                                                               op.utag, 0, nullptr, 0);
         }
         return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
     }
@@ -2108,13 +2113,18 @@ int launch_cascade_x0(double* cols, const double* a, const double* d, const doub
 
 int launch_cascade_panel(double* cols, const double* a, const double* d, idx_t m, idx_t n,
                          idx_t q0, idx_t p0, idx_t p1, double* denoms, int32_t* fail_dev,
-                         int* flags, int epoch, cudaStream_t st, const PeerSet* peers) {
+                         int* flags, int epoch, cudaStream_t st, const PeerSet* peers,
+                         int utag) {
     if (m < 1 || m > INT_MAX / 4 || q0 < 0 || q0 > p0 || p1 > n) return PDAS_ERR_ARG;
     CascOp op;
     op.kind = 1;
     op.q0 = q0;
     op.p0 = p0;
     op.p1 = p1;
+    if (utag > 0) {  // chained: wait for this rank's own update of the tiles
+        op.uflag = flags + (n + 2);
+        op.utag = utag;
+    }
     if (peers) {
         if (peers->count < 0 || peers->count > kMaxPeers) return PDAS_ERR_ARG;
         op.peers = *peers;
@@ -2157,7 +2167,7 @@ int launch_peer_wait(const int* flags, idx_t m, idx_t c0, idx_t c1, int epoch, c
 
 int launch_cascade_update(double* cols, const double* a, const double* d, idx_t m, idx_t n,
                           idx_t p0, idx_t p1, const int64_t* tiles, idx_t ntiles, double* denoms,
-                          int32_t* fail_dev, cudaStream_t st) {
+                          int32_t* fail_dev, cudaStream_t st, int* flags, int utag) {
     if (m < 1 || m > INT_MAX / 4 || p0 < 0 || p1 > n || ntiles < 0) return PDAS_ERR_ARG;
     CascOp op;
     op.kind = 2;
@@ -2165,6 +2175,10 @@ int launch_cascade_update(double* cols, const double* a, const double* d, idx_t 
     op.p1 = p1;
     op.tiles = tiles;
     op.ntiles = ntiles;
+    if (flags && utag > 0) {  // publish tile_done = utag for every tile updated
+        op.uflag = flags + (n + 2);
+        op.utag = utag;
+    }
     return dispatch_cascade(cols, a, d, m, n, denoms, fail_dev, nullptr, 0, kMaxBlock, st, op);
 }
 

@@ -81,7 +81,8 @@ constexpr int kMaxPeers = 7;  // one box: 8 GPUs
 struct PeerSet;              // cascade.cu
 int launch_cascade_panel(double* cols, const double* a, const double* d, idx_t m, idx_t n,
                          idx_t q0, idx_t p0, idx_t p1, double* denoms, int32_t* fail_dev,
-                         int* flags, int epoch, cudaStream_t st, const PeerSet* peers = nullptr);
+                         int* flags, int epoch, cudaStream_t st, const PeerSet* peers = nullptr,
+                         int utag = 0);
 int launch_cascade_panel_peers(double* cols, const double* a, const double* d, idx_t m, idx_t n,
                                idx_t q0, idx_t p0, idx_t p1, double* denoms, int32_t* fail_dev,
                                int* flags, int epoch, int npeers, double* const* peer_cols,
@@ -90,7 +91,7 @@ int launch_cascade_panel_peers(double* cols, const double* a, const double* d, i
 int launch_peer_wait(const int* flags, idx_t m, idx_t c0, idx_t c1, int epoch, cudaStream_t st);
 int launch_cascade_update(double* cols, const double* a, const double* d, idx_t m, idx_t n,
                           idx_t p0, idx_t p1, const int64_t* tiles, idx_t ntiles, double* denoms,
-                          int32_t* fail_dev, cudaStream_t st);
+                          int32_t* fail_dev, cudaStream_t st, int* flags = nullptr, int utag = 0);
 idx_t cascade_supported_m();
 idx_t cascade_flags_count(idx_t m, idx_t n);
 int cascade_tile_width(idx_t m);

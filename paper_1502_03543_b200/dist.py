@@ -117,6 +117,15 @@ class ShardPlan:
         t0 = (last + self.w - 1) // self.w
         return bisect.bisect_left(self._tl, t0)
 
+    def update_start_chained(self, b: int) -> int:
+        """Chained schedule: update(b) also covers block b+1's tiles (the early
+        panel of block b+1 waits for them on its own rank)."""
+        if b + 1 < self.nb:
+            t0 = self.block(b + 1)[0] // self.w
+        else:
+            t0 = (self.block(b)[1] + self.w - 1) // self.w
+        return bisect.bisect_left(self._tl, t0)
+
     def block_op(self, b: int) -> Op:
         c0, c1 = self.block_columns(b)
         p0, p1 = self.block(b)
@@ -144,6 +153,9 @@ class _NullBackend:
     def block_final(self, b: int) -> None:
         pass
 
+    def mark_before_update(self) -> None:
+        pass
+
     def end(self) -> None:
         pass
 
@@ -151,8 +163,17 @@ class _NullBackend:
 def cascade_schedule(plan: ShardPlan, be) -> Iterator[Op]:
     """One sharded cascade on this rank; yields each collective (see module doc).
 
-    `be` provides panel(q0, p0, p1), update(p0, p1, i0) (tiles plan.tiles[i0:])
-    and the stream hooks of _NullBackend."""
+    `be` provides panel(q0, p0, p1, tag), update(p0, p1, i0, tag) (tiles
+    plan.tiles[i0:]) and the stream hooks of _NullBackend.
+
+    be.chained (the 1-GPU engine's early-panel order, r02): update(b) on the
+    owner of block b+1 covers block b+1's tiles first and tags them b+1; the
+    panel of block b+1 then applies no previous block itself (q0 = p0) and
+    waits in-kernel for those tags -- 2B instead of 3B dependent steps per
+    block on the serial chain, the multi-GPU ceiling."""
+    if getattr(be, "chained", False):
+        yield from _chained_schedule(plan, be)
+        return
     be.begin()
     with be.side():
         if plan.owns_block(0):
@@ -171,6 +192,36 @@ def cascade_schedule(plan: ShardPlan, be) -> Iterator[Op]:
         if i0 < len(plan.tiles):
             be.update(*plan.block(b), i0)
         be.mark_update()
+    be.main_wait_side()
+    be.end()
+    if not plan.x_in_last_panel:
+        yield ("x", plan.x_owner)
+
+
+def _chained_schedule(plan: ShardPlan, be) -> Iterator[Op]:
+    be.begin()
+    with be.side():
+        if plan.owns_block(0):
+            p0, p1 = plan.block(0)
+            be.panel(p0, p0, p1, tag=0)
+        yield plan.block_op(0)
+    for b in range(plan.nb):
+        be.main_wait_side()  # block b is final here
+        be.block_final(b)
+        be.mark_before_update()  # the main stream up to update(b-1)
+        i0 = plan.update_start_chained(b)
+        if i0 < len(plan.tiles):
+            be.update(*plan.block(b), i0, tag=b + 1)
+        be.mark_update()
+        if b + 1 < plan.nb:
+            with be.side():
+                if plan.owns_block(b + 1):
+                    # not resident while update(b-1) still runs; waits in-kernel
+                    # for this rank's update(b) of its own tiles
+                    be.side_wait_update()
+                    p0, p1 = plan.block(b + 1)
+                    be.panel(p0, p0, p1, tag=b + 1)
+                yield plan.block_op(b + 1)
     be.main_wait_side()
     be.end()
     if not plan.x_in_last_panel:
@@ -287,6 +338,9 @@ class CudaShard(_NullBackend):
             self.side_stream = t.cuda.Stream(priority=hi)
             self.ev_update = t.cuda.Event()
         self.main = None
+        # the chained (early-panel) schedule for the broadcast exchange; the
+        # experimental fused peer exchange keeps the previous-block panels
+        self.chained = not self.fused
         self.x0_low = x0_low
         x_tile = plan.n // plan.w
         self.xlane = (x0_low is not None and streams and not plan.x_in_last_panel
@@ -296,8 +350,9 @@ class CudaShard(_NullBackend):
             keep = plan.tiles[plan.tiles != x_tile]
             self.tiles = t.from_numpy(keep.copy()).to(dv.device())
             self._ntiles = len(keep)
-            self._starts = [int(np.searchsorted(keep, plan.tiles[plan.update_start(b)])
-                                if plan.update_start(b) < len(plan.tiles) else len(keep))
+            start = plan.update_start_chained if self.chained else plan.update_start
+            self._starts = [int(np.searchsorted(keep, plan.tiles[start(b)])
+                                if start(b) < len(plan.tiles) else len(keep))
                             for b in range(plan.nb)]
             self.x_tiles = t.tensor([x_tile], dtype=t.int64, device=dv.device())
             self.x_stream = t.cuda.Stream(priority=hi)
@@ -316,6 +371,9 @@ class CudaShard(_NullBackend):
         self.epoch += 1
         if not self.fused:  # fused: the caller zeroes it before the peers may write it
             self.fail.zero_()
+        if self.chained:
+            self.call("pdas_cascade_reset_tags", self.dv.ptr(self.ws), self.plan.n,
+                      self.dv.stream())
         if self.streams:
             self.main = self.t.cuda.current_stream()
             self.side_stream.wait_stream(self.main)
@@ -361,12 +419,21 @@ class CudaShard(_NullBackend):
             self.side_stream.wait_event(self.ev_update)
 
     def mark_update(self) -> None:
+        if self.streams and not self.chained:
+            self.ev_update.record(self.main)
+
+    def mark_before_update(self) -> None:
         if self.streams:
             self.ev_update.record(self.main)
 
     # -- compute
-    def panel(self, q0: int, p0: int, p1: int) -> None:
+    def panel(self, q0: int, p0: int, p1: int, tag: int = 0) -> None:
         p, dv = self.plan, self.dv
+        if self.chained:
+            self.call("pdas_cascade_panel_chained", dv.ptr(self.cols), dv.ptr(self.a),
+                      dv.ptr(self.d), p.m, p.n, p0, p1, dv.ptr(self.ws), self.epoch,
+                      dv.ptr(self.fail), tag, dv.stream())
+            return
         if self.fused:
             pc, pw, pf = self._peer_arrays
             self.call("pdas_cascade_panel_peers", dv.ptr(self.cols), dv.ptr(self.a),
@@ -387,11 +454,16 @@ class CudaShard(_NullBackend):
         self.call("pdas_cascade_peer_wait", dv.ptr(self.ws), p.m, p.n, c0, c1, self.epoch,
                   dv.stream())
 
-    def update(self, p0: int, p1: int, i0: int) -> None:
+    def update(self, p0: int, p1: int, i0: int, tag: int = 0) -> None:
         p, dv = self.plan, self.dv
         if self._starts is not None:  # x lane: index into the list without the x tile
             i0 = self._starts[p0 // p.B]
         if i0 >= self._ntiles:
+            return
+        if tag > 0:
+            self.call("pdas_cascade_update_tagged", dv.ptr(self.cols), dv.ptr(self.a),
+                      dv.ptr(self.d), p.m, p.n, p0, p1, dv.ptr(self.tiles) + 8 * i0,
+                      self._ntiles - i0, dv.ptr(self.ws), dv.ptr(self.fail), tag, dv.stream())
             return
         self.call("pdas_cascade_update", dv.ptr(self.cols), dv.ptr(self.a), dv.ptr(self.d), p.m,
                   p.n, p0, p1, dv.ptr(self.tiles) + 8 * i0, self._ntiles - i0, dv.ptr(self.ws),

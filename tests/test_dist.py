@@ -115,10 +115,25 @@ def _breakdown_d(a, d, cols, step):
     return d2
 
 
-def _lockstep(a, d, cols, world, B, w):
+class ChainedOracleShard(OracleShard):
+    """The chained (early-panel) schedule: update(b) covers block b+1's tiles,
+    the panel applies no previous block (the GPU form waits on tile tags)."""
+
+    chained = True
+
+    def panel(self, q0, p0, p1, tag=0):
+        assert q0 == p0
+        super().panel(q0, p0, p1)
+
+    def update(self, p0, p1, i0, tag=0):
+        super().update(p0, p1, i0)
+
+
+def _lockstep(a, d, cols, world, B, w, chained=False):
     m, n = a.shape
     plans = [D.ShardPlan(m, n, world, r, B, w) for r in range(world)]
-    bes = [OracleShard(p, cols, a, d) for p in plans]
+    cls = ChainedOracleShard if chained else OracleShard
+    bes = [cls(p, cols, a, d) for p in plans]
     D.run_lockstep(plans, bes)
     return [int(be.fail[0]) for be in bes], [be.cols for be in bes]
 
@@ -142,11 +157,12 @@ def test_plan_ownership():
     (5, 1, 2, 2, 1), (5, 7, 2, 2, 1), (7, 45, 2, 4, 2), (7, 40, 2, 8, 4), (9, 41, 3, 8, 4),
     (6, 64, 4, 16, 8), (12, 63, 5, 8, 8), (3, 30, 1, 4, 2), (16, 100, 3, 16, 16),
 ])
-def test_lockstep_bitwise(m, n, world, B, w):
+@pytest.mark.parametrize("chained", [False, True])
+def test_lockstep_bitwise(m, n, world, B, w, chained):
     a, d, cols = _system(m, n, 31 * m + n)
     ret, ref = _serial(a, d, cols)
     assert ret == 0
-    fails, outs = _lockstep(a, d, cols, world, B, w)
+    fails, outs = _lockstep(a, d, cols, world, B, w, chained)
     assert fails == [0] * world
     for c in outs:
         assert bits_equal(c, ref)
@@ -161,6 +177,8 @@ def test_lockstep_breakdown(step):
     assert ret == step + 1
     fails, _ = _lockstep(a, d, cols, 3, 4, 2)
     assert fails == [step + 1] * 3
+    fails, _ = _lockstep(a, d, cols, 3, 4, 2, chained=True)
+    assert fails == [step + 1] * 3
 
 
 def _free_port():
@@ -171,7 +189,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, cases):
+def _worker(rank, world, port, cases, chained=False):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -184,7 +202,7 @@ def _worker(rank, world, port, cases):
                 d = _breakdown_d(a, d, cols, step)
             ret, ref = _serial(a, d, cols)
             plan = D.ShardPlan(m, n, world, rank, B, w)
-            be = OracleShard(plan, cols, a, d)
+            be = (ChainedOracleShard if chained else OracleShard)(plan, cols, a, d)
             D.run_collective(plan, be)
             assert int(be.fail[0]) == ret, (m, n, rank, int(be.fail[0]), ret)
             if ret == 0:
@@ -194,13 +212,13 @@ def _worker(rank, world, port, cases):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_gloo_processes_bitwise(world):
+@pytest.mark.parametrize("world,chained", [(2, False), (3, False), (2, True), (3, True)])
+def test_gloo_processes_bitwise(world, chained):
     import torch.multiprocessing as mp
 
     cases = [(7, 45, 4, 2, 1, None), (8, 40, 8, 4, 2, None), (5, 33, 8, 8, 3, None),
              (6, 41, 4, 2, 7, 22)]
-    mp.spawn(_worker, args=(world, _free_port(), cases), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), cases, chained), nprocs=world, join=True)
 
 
 class FusedOracleShard(OracleShard):
