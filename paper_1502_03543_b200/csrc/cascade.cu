@@ -1079,8 +1079,10 @@ __global__ void __launch_bounds__(TC + 128, TC == 128 ? 2 : 1)
                      int need, const int* __restrict__ pflag, int epoch) {
     static_assert(TC == 256 || TC == 128, "compute threads");
     constexpr bool kLdg = R <= 4;
-    constexpr int kRegC = TC == 256 ? kWsRegsCompute : (kLdg ? 208 : 216);
-    constexpr int kRegR = TC == 256 ? kWsRegsReducer : (kLdg ? 48 : 40);
+    // TC = 128 direct-load: 224/32 (208/48 spilled ~170 B in the pivot loop;
+    // c4 cascade 2103 -> 1929 ms, c5 32.4 -> 31.3 ms)
+    constexpr int kRegC = TC == 256 ? kWsRegsCompute : (kLdg ? 224 : 216);
+    constexpr int kRegR = TC == 256 ? kWsRegsReducer : (kLdg ? 32 : 40);
     double *red, *bc;
     Pipe<S> pp;
     carve<TC, C, 1, S>(red, bc, pp, false, m);
@@ -1445,7 +1447,11 @@ __global__ void __launch_bounds__(T + PW, 1)
             NCH > 1 ? flags + tile * NCH : nullptr, epoch, hop_con, PW > 0 ? &s_pub : nullptr);
         HOP_MARK(hop_pub, 0);
         if (!broken) {
-            tl.store(cols, col0, n + 1);
+            // the earlier chunks went out mid-triangle (a chunk goes out iff it
+            // ends before the tile's last pivot): store only the rest
+            const int cnt = (int)((col0 + C < p1 ? col0 + C : p1) - col0);
+            const int first = NCH > 1 ? (cnt - 1) / CH * CH : 0;
+            tl.store(cols, col0, n + 1, first, C);
             stored = true;
         }
 #if PDAS_PANEL_TRACE
@@ -1824,7 +1830,8 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
                                                                            : 0;
     const size_t smem_p = casc_smem_bytes<TP, CT, 1>(sp, m);
     auto ku = k_casc_update<TMA, S, T, R, Cu, G, GEN>;
-    // a publisher warp where the registers allow it (TP <= 256: c2, c4, c5)
+    // a publisher warp where the registers allow it (TP <= 256: c2, c4, c5;
+    // 512 + 32 threads are allocated as 20 warps -> 96 registers, spills)
     constexpr int PW = (TP <= 256 && !GEN) ? 32 : 0;
     constexpr int TPB = TP + PW;  // panel block size
     auto kp = sp == 4   ? k_casc_panel<!GEN, 4, TP, RP, CT, GEN, PW>
