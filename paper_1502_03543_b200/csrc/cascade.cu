@@ -1520,7 +1520,9 @@ __global__ void k_peer_wait(const int* __restrict__ flags, idx_t t0, idx_t t1, i
 // Computing inner_k then updating column k per column equals the reference's
 // phase 1 / phase 2 split (_kernels.pyx:247-266): the pivot column is not
 // written in step l.
-constexpr int kSmallThreads = 256;
+// 512 threads: 64 column groups, ~1.6 passes per step at c1 (256: 0.37 ms per
+// c1 cascade, 512: 0.32, 1024: 0.50 -- 64 registers spill the tile)
+constexpr int kSmallThreads = 512;
 constexpr int KB = 1;  // columns per group and pass (k_casc_small; 2 and 4 measured slower)
 
 // shared-memory column stride: m rounded up to 8 (mod 16) doubles, so the four
@@ -1529,13 +1531,64 @@ __host__ __device__ inline idx_t small_stride(idx_t m) { return (m + 7) / 16 * 1
 
 __host__ __device__ inline size_t small_cascade_smem(idx_t m, idx_t n) {
     const idx_t mp = small_stride(m);
-    return (size_t)((n + 1) * mp + n * mp + n) * sizeof(double);
+    return (size_t)((n + 1) * mp + n * mp + n + mp) * sizeof(double);  // + x0 scratch
+}
+
+// x0 = L^-T L^-1 rhs for column x of [Y | x] in shared memory, by one warp
+// (m <= 64: rows lane and lane + 32), with exactly the operations of
+// k_fwd_one / k_bwd_one (solve_kernels.cu): forward column sweeps
+// x_j /= L_jj, x_i -= L_ij x_j; backward rows s = y_r - L_{r+1,r} x_{r+1}
+// - L_{r+2,r} x_{r+2} - ... in ascending order, x_r = s / L_rr.  q: m doubles.
+__device__ __forceinline__ void small_x0_warp(const double* __restrict__ L, int m, double* x,
+                                              double* q) {
+    const int lane = threadIdx.x & 31;
+    double xr[2];
+    for (int k = 0; k < 2; ++k) xr[k] = lane + 32 * k < m ? x[lane + 32 * k] : 0.0;
+    for (int j = 0; j < m; ++j) {
+        const int owner = j & 31, slot = j >> 5;
+        double l[2];
+        for (int k = 0; k < 2; ++k) {
+            const int i = lane + 32 * k;
+            l[k] = i < m ? __ldg(L + (size_t)j * m + i) : 0.0;
+        }
+        if (lane == owner) xr[slot] = xr[slot] / l[slot];
+        const double xj = __shfl_sync(0xffffffffu, xr[slot], owner);
+        for (int k = 0; k < 2; ++k) {
+            const int i = lane + 32 * k;
+            if (i > j && i < m) {
+                const double p = l[k] * xj;
+                xr[k] = xr[k] - p;
+            }
+        }
+    }
+    for (int k = 0; k < 2; ++k)
+        if (lane + 32 * k < m) x[lane + 32 * k] = xr[k];
+    __syncwarp();
+    for (int r = m - 1; r >= 0; --r) {
+        const double* lc = L + (size_t)r * m;  // column r: L_jr at lc[j]
+        for (int j = r + 2 + lane; j < m; j += 32) {
+            const double p = __ldg(lc + j) * x[j];
+            q[j] = p;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            double s = x[r];
+            if (r + 1 < m) {
+                const double p = __ldg(lc + r + 1) * x[r + 1];
+                s = s - p;
+            }
+            for (int j = r + 2; j < m; ++j) s = s - q[j];
+            x[r] = s / __ldg(lc + r);
+        }
+        __syncwarp();
+    }
 }
 
 template <int LPC, int RPL>
 __global__ void __launch_bounds__(kSmallThreads, 1)
     k_casc_small(double* __restrict__ cols, const double* __restrict__ a,
-                 const double* __restrict__ d, int m, int n, int32_t* __restrict__ fail) {
+                 const double* __restrict__ d, int m, int n, int32_t* __restrict__ fail,
+                 const double* __restrict__ x0_low) {
     extern __shared__ __align__(16) double smx[];
     const int mp = (int)small_stride(m);
     double* sc = smx;                          // [n + 1][mp]
@@ -1549,6 +1602,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     for (idx_t e = tid; e < (idx_t)n * m; e += kSmallThreads) sa[(e / m) * mp + e % m] = __ldg(a + e);
     for (int i = tid; i < n; i += kSmallThreads) sdv[i] = __ldg(d + i);
     __syncthreads();
+    if (x0_low) {  // the initial x column (init_workspace's x0 solve) first
+        if (tid < 32) small_x0_warp(x0_low, m, sc + (size_t)n * mp, sdv + n);
+        __syncthreads();
+    }
     const bool m1 = m == 1;
     const int H = m > 1 ? (int)(pow2_ceil(m) >> 1) : 0;
     // rows of this lane: lo = j + LPC r, hi = lo + H (absent rows: +0.0 terms)
@@ -1647,24 +1704,26 @@ static bool small_cascade_fits(idx_t m, idx_t n) {
 
 template <int LPC, int RPL>
 static int launch_small(double* cols, const double* a, const double* d, idx_t m, idx_t n,
-                        int32_t* fail, cudaStream_t st) {
+                        int32_t* fail, const double* x0_low, cudaStream_t st) {
     const size_t smem = small_cascade_smem(m, n);
     cudaFuncSetAttribute(k_casc_small<LPC, RPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    k_casc_small<LPC, RPL><<<1, kSmallThreads, smem, st>>>(cols, a, d, (int)m, (int)n, fail);
+    k_casc_small<LPC, RPL><<<1, kSmallThreads, smem, st>>>(cols, a, d, (int)m, (int)n, fail,
+                                                           x0_low);
     return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
 }
 
-// groups of 8 lanes per column (up to 4 s-indices each); fewer for H < 8
+// groups of 8 lanes per column (up to 4 s-indices each); fewer for H < 8.
+// x0_low: solve the x column in the kernel first (launch_cascade_x0)
 static int launch_small_cascade(double* cols, const double* a, const double* d, idx_t m, idx_t n,
-                                int32_t* fail, cudaStream_t st) {
+                                int32_t* fail, cudaStream_t st, const double* x0_low = nullptr) {
     const idx_t H = m > 1 ? pow2_ceil(m) >> 1 : 0;
-    if (H == 32) return launch_small<8, 4>(cols, a, d, m, n, fail, st);
-    if (H == 16) return launch_small<8, 2>(cols, a, d, m, n, fail, st);
-    if (H == 8) return launch_small<8, 1>(cols, a, d, m, n, fail, st);
-    if (H == 4) return launch_small<4, 1>(cols, a, d, m, n, fail, st);
-    if (H == 2) return launch_small<2, 1>(cols, a, d, m, n, fail, st);
-    return launch_small<1, 1>(cols, a, d, m, n, fail, st);  // m <= 2
+    if (H == 32) return launch_small<8, 4>(cols, a, d, m, n, fail, x0_low, st);
+    if (H == 16) return launch_small<8, 2>(cols, a, d, m, n, fail, x0_low, st);
+    if (H == 8) return launch_small<8, 1>(cols, a, d, m, n, fail, x0_low, st);
+    if (H == 4) return launch_small<4, 1>(cols, a, d, m, n, fail, x0_low, st);
+    if (H == 2) return launch_small<2, 1>(cols, a, d, m, n, fail, x0_low, st);
+    return launch_small<1, 1>(cols, a, d, m, n, fail, x0_low, st);  // m <= 2
 }
 
 // ------------------------------------------------------------ host side
@@ -2107,10 +2166,8 @@ int launch_cascade_x0(double* cols, const double* a, const double* d, const doub
     if (m < 1 || n < 0 || m > INT_MAX / 4) return PDAS_ERR_ARG;
     cudaMemsetAsync(fail_dev, 0, sizeof(int32_t), st);
     if (n == 0) return launch_solve_one(low, m, cols, work, st);
-    if (small_cascade_fits(m, n)) {  // x0 first, then the one-CTA cascade
-        const int rc = launch_solve_one(low, m, cols + (size_t)n * m, work, st);
-        return rc ? rc : launch_small_cascade(cols, a, d, m, n, fail_dev, st);
-    }
+    if (small_cascade_fits(m, n))  // x0 solved inside the one-CTA cascade, first
+        return launch_small_cascade(cols, a, d, m, n, fail_dev, st, low);
     CascOp op;
     op.x0_low = low;
     op.x0_work = work;

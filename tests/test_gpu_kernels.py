@@ -202,8 +202,8 @@ def test_hoisted_division_bits(gpu):
     del torch
 
 
-@pytest.mark.parametrize("m,n", [(50, 200), (50, 203), (300, 1024), (300, 1030), (1000, 2048),
-                                 (1000, 2050)])
+@pytest.mark.parametrize("m,n", [(1, 4), (2, 9), (7, 30), (33, 70), (64, 100), (50, 200),
+                                 (50, 203), (300, 1024), (300, 1030), (1000, 2048), (1000, 2050)])
 def test_cascade_with_fused_x0(gpu, m, n):
     """pdas_solve_sweeps_ws_x0: x0 = L0^-T L0^-1 rhs solved inside the cascade
     call (overlapped on its own stream when column n is alone in the last tile,
