@@ -49,7 +49,7 @@ namespace pdas {
 #define PDAS_HOP_TRACE 0
 #endif
 #if PDAS_HOP_TRACE
-__device__ unsigned long long g_hop_trace[16];
+__device__ unsigned long long g_hop_trace[32];
 #define HOP_MARK(cond, k)                                                          \
     do {                                                                           \
         if ((cond) && threadIdx.x == 0) {                                          \
@@ -58,9 +58,20 @@ __device__ unsigned long long g_hop_trace[16];
             g_hop_trace[k] = t_;                                                   \
         }                                                                          \
     } while (0)
+#define PW_MARK(cond, k)                                                           \
+    do {                                                                           \
+        if (cond) {                                                                \
+            unsigned long long t_;                                                 \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+            g_hop_trace[k] = t_;                                                   \
+        }                                                                          \
+    } while (0)
 #else
 #define HOP_MARK(cond, k) \
     do {                  \
+    } while (0)
+#define PW_MARK(cond, k) \
+    do {                 \
     } while (0)
 #endif
 #if PDAS_PANEL_TRACE
@@ -1492,6 +1503,313 @@ __global__ void __launch_bounds__(T + PW, 1)
     HOP_MARK(hop_pub, 2);
 }
 
+// ------------------------------------------------------------ warp-per-column panel
+// The panel as a latency chain of 8-column tiles (c2, c3, c5: 64 <= H <= 1024,
+// one pivot block, nothing of the previous block left to apply).  Each of the
+// tile's columns lives in ONE warp (Tile<32, H/32, 1>: rows lane + 32 r and
+// + H, the same reference tree: in-lane levels, then the 32-lane butterfly),
+// so a pivot step needs no CTA barrier: each warp reduces, divides and updates
+// its own column as soon as the pivot's [P | A] stage has landed.  A ninth
+// warp is the producer: it acquires the earlier tiles' chunk flags, stages
+// their denominators and streams [P_l | A_l] (A_l alone for the tile's own
+// pivots) through an S-stage bulk-copy ring (full: producer arrive + bytes,
+// empty: one arrival per column warp).  Triangle step cl: warp cl writes its
+// final column into the stage's P half, reduces its own denominator and
+// releases tri[cl]; warps c > cl reduce their columns meanwhile and apply the
+// step after tri[cl].  Chunk 0 (columns 0..3) is published by the last of its
+// four warps to finish (shared-memory count, one gpu-scope fence), the rest at
+// the end.  Breakdown and a failed earlier tile keep the stage protocol going
+// with the arithmetic skipped, so no warp waits on a stage that never comes.
+constexpr int kPwCols = 8;                        // columns per tile (CT)
+// + a producer warpgroup (one active lane) that hands its registers to the
+// column warps: 168 at launch, column warps 232, producer warpgroup 40 (the
+// 64-double column of H = 1024 does not fit 168 without spills)
+constexpr int kPwThreads = 32 * kPwCols + 128;
+
+__host__ __device__ inline size_t panel_w_smem(int S, int m) {
+    const size_t mp = (size_t)((m + 1) & ~1);
+    return (size_t)S * 2 * mp * 8 + 3 * (size_t)kMaxBlock * 8 + kPwCols * 8 + kPwCols * 4 +
+           (2 * (size_t)S + kPwCols) * 8 + 16;
+}
+
+template <int R, int S, bool FULL>
+__global__ void __launch_bounds__(kPwThreads, 1)
+    k_casc_panel_w(double* __restrict__ cols, const double* __restrict__ a,
+                   const double* __restrict__ d, double* __restrict__ denoms, int m, idx_t n,
+                   idx_t p0, idx_t p1, int32_t* __restrict__ fail, int* __restrict__ flags,
+                   int epoch, const int* __restrict__ uflag, int utag) {
+    constexpr int C = kPwCols, CH = C / kPanelChunks, NCH = kPanelChunks;
+    const idx_t tile = p0 / C + blockIdx.x;
+    if (__syncthreads_or(threadIdx.x == 0 && *(volatile int32_t*)fail != 0)) {
+        if (threadIdx.x == 0)
+            for (int ch = 0; ch < NCH; ++ch) st_release(flags + tile * NCH + ch, epoch);
+        return;
+    }
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int mp = (m + 1) & ~1;
+    double* buf = reinterpret_cast<double*>(smem_raw);  // S x [P | A]
+    double* sd = buf + (size_t)S * 2 * mp;               // d, window base p0
+    double* sden = sd + kMaxBlock;                       // earlier tiles' denominators
+    double* sy = sden + kMaxBlock;                       // and their div_recip
+    double* stden = sy + kMaxBlock;                      // this tile's denominators
+    int* stbrk = reinterpret_cast<int*>(stden + C);      // step cl broke down
+    uint64_t* full = reinterpret_cast<uint64_t*>(stbrk + C);
+    uint64_t* empty = full + S;
+    uint64_t* tri = empty + S;
+    int* s_state = reinterpret_cast<int*>(tri + C);      // [0] dead, [1] chunk-0 count
+    const uint32_t full_a = smem_addr(full), empty_a = smem_addr(empty), tri_a = smem_addr(tri);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, C);
+        }
+        for (int k = 0; k < C; ++k) mbar_init(tri + k, 1);
+        s_state[0] = 0;
+        s_state[1] = 0;
+        mbar_fence_init();
+    }
+    for (idx_t l = p0 + threadIdx.x; l < p1; l += blockDim.x) sd[l - p0] = __ldg(d + l);
+    // this tile's last update (the previous block's update kernel, running
+    // concurrently) must have landed before the tile is read
+    if (uflag && threadIdx.x == 0)
+        while (ld_acquire(uflag + tile) != utag) {
+            if (*(volatile int32_t*)fail) break;
+            __nanosleep(64);
+        }
+    const bool dead0 =
+        __syncthreads_or(uflag != nullptr && threadIdx.x == 0 && *(volatile int32_t*)fail != 0);
+    const idx_t col0 = tile * C;
+    const int cnt = (int)((col0 + C < p1 ? col0 + C : p1) - col0);
+    const idx_t ncols = n + 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t bytes = (uint32_t)m * 8u;
+    const bool hop_pub = gridDim.x == 32 && blockIdx.x == 15 && p0 == 5 * (p1 - p0);
+    const bool hop_con = gridDim.x == 32 && blockIdx.x == 16 && p0 == 5 * (p1 - p0);
+    (void)hop_pub;
+    (void)hop_con;
+    if (warp >= C) {
+        // ---- producer warpgroup (one lane works)
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+        if (warp == C && !dead0) {
+            unsigned use = 0;
+            bool dead = false;
+            auto issue = [&](idx_t l, bool with_p) {  // lane 0
+                const uint32_t sl = use % S;
+                if (use >= (unsigned)S) mbar_wait_a(empty_a + 8 * sl, ((use / S) - 1u) & 1u);
+                const uint32_t fb = full_a + 8 * sl;
+                if (dead) {
+                    mbar_arrive_a(fb);  // drain: the column warps skip the step
+                } else {
+                    double* dst = buf + (size_t)sl * 2 * mp;
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
+                                 "r"(with_p ? 2 * bytes : bytes)
+                                 : "memory");
+                    if (with_p) tma_load_1d(dst, cols + l * m, bytes, full + sl);
+                    tma_load_1d(dst + mp, a + l * m, bytes, full + sl);
+                }
+                ++use;
+            };
+            for (idx_t tp = p0 / C; tp < tile; ++tp) {
+                // the previous tile chunk by chunk (its triangle may still run);
+                // older tiles are complete: one wait on their last chunk
+                const bool prev = tp == tile - 1;
+                for (int ch = prev ? 0 : NCH - 1; ch < NCH; ++ch) {
+                    const idx_t pa = tp * C + (prev ? ch * CH : 0);
+                    const idx_t pe = tp * C + (ch + 1) * CH;
+                    const idx_t pb = pe < p1 ? pe : p1;
+                    if (!dead) {
+                        int f = 0;
+                        if (lane == 0) {
+                            while (ld_acquire(flags + tp * NCH + ch) != epoch) __nanosleep(32);
+                            PW_MARK(hop_con && prev && ch == NCH - 1, 2);
+                            f = *(volatile int32_t*)fail;
+                            if (f) *(volatile int*)s_state = 1;
+                            else fence_proxy_async_global();  // their stores -> our bulk reads
+                        }
+                        dead = __shfl_sync(0xffffffffu, f, 0) != 0;
+                        // the chunk's denominators, one lane per pivot (after the
+                        // flag: __syncwarp orders lane 0's acquire before the loads)
+                        __syncwarp();
+                        if (!dead)
+                            for (idx_t l = pa + lane; l < pb; l += 32) {
+                                const double den = __ldcg(denoms + l);
+                                sden[l - p0] = den;
+                                sy[l - p0] = div_recip(den);
+                            }
+                        __syncwarp();
+                        PW_MARK(hop_con && prev && ch == NCH - 1 && lane == 0, 3);
+                    }
+                    if (lane == 0)
+                        for (idx_t l = pa; l < pb; ++l)
+                            if (sd[l - p0] != 1.0) issue(l, true);  // _kernels.pyx:242-243
+                    __syncwarp();
+                }
+            }
+            if (lane == 0)
+                for (int cl = 0; cl < cnt; ++cl)
+                    if (sd[col0 + cl - p0] != 1.0) issue(col0 + cl, false);
+        }
+    } else {
+        // ---- column warp: column col0 + warp of the tile
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+        const idx_t col = col0 + warp;
+        const bool have = col < ncols;
+        Tile<32, R, 1, false> tl;
+        tl.init(lane, m, 0, nullptr, nullptr);
+        const int H = tl.H;
+        if (have && !dead0) tl.load(cols, col, ncols);
+        // inner product of v = A_l (d_l - 1) with this column (reference tree)
+        auto dot = [&](const double* ac, double f) {
+            const double t = stream_tree<R>([&](int r) {
+                const int row = lane + 32 * r;
+                const double vl = ac[row] * f;
+                const double lo = vl * tl.xl[r][0];
+                const double vh = (FULL || tl.vhi(r)) ? ac[row + H] * f : 0.0;
+                const double hi = vh * tl.xh[r][0];
+                return lo + hi;
+            });
+            return warp_butterfly32(t);
+        };
+        auto axpy = [&](double g, const double* pc) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int row = lane + 32 * r;
+                const double q0 = g * pc[row];
+                tl.xl[r][0] = tl.xl[r][0] - q0;
+                if (FULL || tl.vhi(r)) {
+                    const double q1 = g * pc[row + H];
+                    tl.xh[r][0] = tl.xh[r][0] - q1;
+                }
+            }
+        };
+        unsigned use = 0;
+        bool dead = dead0, broken = false, stored = false;
+#if PDAS_HOP_TRACE
+        const bool acc = hop_con && lane == 0 && (warp == 0 || warp == C - 1);
+        const int ab = warp == 0 ? 16 : 24;
+        long long tw = clock64();
+#define PW_ACC(k)                                             \
+    do {                                                      \
+        if (acc) {                                            \
+            const long long tn = clock64();                   \
+            g_hop_trace[ab + (k)] += (unsigned long long)(tn - tw); \
+            tw = tn;                                          \
+        }                                                     \
+    } while (0)
+#else
+#define PW_ACC(k) \
+    do {          \
+    } while (0)
+#endif
+        auto wait_stage = [&](uint32_t& sl) {
+            sl = use % S;
+            PW_ACC(0);  // work since the last mark
+            mbar_wait_a(full_a + 8 * sl, (use / S) & 1u);
+            PW_ACC(1);  // stage wait
+            if (!dead) dead = *(volatile int*)s_state != 0;
+        };
+        auto release_stage = [&](uint32_t sl) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive_a(empty_a + 8 * sl);
+            ++use;
+        };
+        if (!dead0) {
+            // earlier tiles' pivots, ascending
+            for (idx_t l = p0; l < col0; ++l) {
+                const double dl = sd[l - p0];
+                if (dl == 1.0) continue;
+                uint32_t sl;
+                wait_stage(sl);
+                PW_MARK(hop_con && warp == 0 && lane == 0 && l == col0 - CH, 9);
+                if (!dead && have) {
+                    const double* pc = buf + (size_t)sl * 2 * mp;
+                    const double inner = dot(pc + mp, dl - 1.0);
+                    const double g = div_by(inner, sden[l - p0], sy[l - p0]);
+                    axpy(g, pc);
+                }
+                release_stage(sl);
+            }
+            PW_ACC(0);
+#if PDAS_HOP_TRACE
+            if (acc) g_hop_trace[ab + 3] += (unsigned long long)(col0 - p0);  // apply steps
+#endif
+            PW_MARK(hop_con && warp == 0 && lane == 0, 4);
+            // the triangle over the tile's own pivots
+            const bool mid = cnt > CH;  // chunk 0 goes out before the triangle ends
+            for (int cl = 0; cl < cnt; ++cl) {
+                const idx_t l = col0 + cl;
+                const double dl = sd[l - p0];
+                if (dl != 1.0) {  // _kernels.pyx:242-243
+                uint32_t sl;
+                wait_stage(sl);
+                double* pc = buf + (size_t)sl * 2 * mp;
+                const bool live = !dead && !broken;
+                if (warp == cl) {
+                    int brk = broken ? 1 : 0;
+                    if (live) {
+#pragma unroll
+                        for (int r = 0; r < R; ++r) {  // P_l for the later columns
+                            pc[lane + 32 * r] = tl.xl[r][0];
+                            if (FULL || tl.vhi(r)) pc[lane + 32 * r + H] = tl.xh[r][0];
+                        }
+                        const double inner = dot(pc + mp, dl - 1.0);
+                        const double denom = 1.0 + inner;
+                        if (fabs(denom) <= kDenomEpsRel * (1.0 + fabs(inner))) {
+                            brk = 1;
+                            broken = true;
+                            if (lane == 0) *fail = (int32_t)(l + 1);
+                        } else if (lane == 0) {
+                            denoms[l] = denom;
+                            stden[cl] = denom;
+                        }
+                    }
+                    if (lane == 0) stbrk[cl] = brk;
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_a(tri_a + 8 * cl);
+                    PW_MARK(hop_con && lane == 0 && (cl == 0 || cl == C - 1), cl == 0 ? 5 : 7);
+                } else if (warp > cl) {
+                    double inner = 0.0;
+                    if (live && have) inner = dot(pc + mp, dl - 1.0);
+                    PW_ACC(0);
+                    mbar_wait_a(tri_a + 8 * cl, 0);
+                    PW_ACC(2);  // triangle hand-off wait
+                    if (stbrk[cl]) broken = true;
+                    if (!dead && !broken && have) axpy(inner / stden[cl], pc);
+                }
+                release_stage(sl);
+                }
+                if (cl == warp && mid && warp < CH && !dead && !broken) {
+                    // column and denominator final: store the column; the last
+                    // of the chunk's warps releases the chunk flag (shared
+                    // count, then one cumulative gpu-scope fence)
+                    tl.store(cols, col, ncols);
+                    __syncwarp();
+                    if (lane == 0) {
+                        __threadfence_block();
+                        if (atomicAdd(s_state + 1, 1) == CH - 1) {
+                            __threadfence();
+                            st_relaxed(flags + tile * NCH, epoch);
+                            PW_MARK(hop_con, 6);
+                        }
+                    }
+                    stored = true;
+                }
+            }
+            PW_ACC(0);
+            if (!stored && !dead && !broken && have) tl.store(cols, col, ncols);
+        }
+    }
+    // the remaining columns are stored: one gpu-scope fence after the CTA
+    // barrier covers every warp's stores (cumulative), then the chunk flags
+    __syncthreads();
+    PW_MARK(threadIdx.x == 0 && (hop_pub || hop_con), hop_pub ? 0 : 8);
+    if (threadIdx.x == 0) {
+        __threadfence();
+        for (int ch = 0; ch < NCH; ++ch) st_relaxed(flags + tile * NCH + ch, epoch);
+    }
+    PW_MARK(threadIdx.x == 0 && hop_pub, 1);
+}
+
 // Non-owner side of the fused exchange: wait until every tile of columns
 // [c0, c1) has been signalled by its owner's panel for this epoch.  Bounded:
 // a peer that never signals traps after 30 s instead of hanging the device.
@@ -1913,6 +2231,29 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
     constexpr bool use_ws = kUseWs;
     if (use_ws)
         cudaFuncSetAttribute(kws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ws);
+    // the warp-per-column panel (k_casc_panel_w) for the 1-GPU chain, m <= 1024:
+    // every column warp reads each pivot's [P | A] in full, 8x the shared-memory
+    // traffic of the CTA-wide panel -- at H = 1024 (c3) that is ~2000 cycles of
+    // shared bandwidth per step and the two panels tie (163.7 vs 164.0 ms)
+    constexpr int RPW = T * R / 32;  // H / 32
+    constexpr bool kPwOk = !GEN && CT == kPwCols && G == 1 && RPW >= 2 && RPW <= 16;
+    constexpr int SPW = 8;
+    const bool pw = kPwOk && pok && panel_w_smem(SPW, m) <= kPanelSmem;
+    const bool pw_full = m == 2 * (T * R);
+    auto kpw = pw_full ? k_casc_panel_w<kPwOk ? RPW : 2, SPW, true>
+                       : k_casc_panel_w<kPwOk ? RPW : 2, SPW, false>;
+    const size_t smem_w = panel_w_smem(SPW, m);
+    if (pw) cudaFuncSetAttribute(kpw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_w);
+    // panel of block [p0, p1) on stream s_ (nothing of an earlier block pending)
+    auto panel = [&](cudaStream_t s_, idx_t p0_, idx_t p1_, const int* uf, int ut) {
+        const unsigned nt_ = (unsigned)((p1_ - p0_ + CT - 1) / CT);
+        if (pw)
+            kpw<<<nt_, kPwThreads, smem_w, s_>>>(cols, a, d, denoms, m, n, p0_, p1_, fail, flags,
+                                                 epoch, uf, ut);
+        else
+            kp<<<nt_, TPB, smem_p, s_>>>(cols, a, d, denoms, m, n, p0_, p0_, p1_, fail, flags,
+                                         epoch, uf, ut, PeerSet{});
+    };
     const idx_t ntiles = (n + 1 + CT - 1) / CT;
     if (op.kind == 1) {
         if (op.p0 % CT || op.p1 <= op.p0 || op.p1 - op.q0 > 2 * kMaxBlock) return PDAS_ERR_ARG;
@@ -1972,9 +2313,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
             }
         }
         prof.mark(ss.ps, 1, 0, 0);
-        kp<<<(unsigned)tiles_of(0), TPB, smem_p, ss.ps>>>(cols, a, d, denoms, m, n, 0, 0,
-                                                        blk_end(0), fail, flags, epoch, nullptr, 0,
-                                                        PeerSet{});
+        panel(ss.ps, 0, blk_end(0), nullptr, 0);
         prof.mark(ss.ps, 1, 0, 1);
         cudaEventRecord(ss.eP, ss.ps);
         if (xlane) {
@@ -2036,9 +2375,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
                 const idx_t p0 = (b + 1) * B;
                 cudaStreamWaitEvent(ss.ps, ss.eU, 0);
                 prof.mark(ss.ps, 1, b + 1, 0);
-                kp<<<(unsigned)tiles_of(b + 1), TPB, smem_p, ss.ps>>>(
-                    cols, a, d, denoms, m, n, p0, p0, blk_end(b + 1), fail, flags, epoch, uflag,
-                    (int)(b + 1), PeerSet{});
+                panel(ss.ps, p0, blk_end(b + 1), uflag, (int)(b + 1));
                 prof.mark(ss.ps, 1, b + 1, 1);
                 cudaEventRecord(ss.eP, ss.ps);
                 if (xlane) {

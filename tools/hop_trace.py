@@ -20,6 +20,8 @@ from paper_1502_03543_b200._lib import call, load  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--m", type=int, default=500)
 ap.add_argument("--n", type=int, default=5000)
+ap.add_argument("--legacy", action="store_true",
+                help="the CTA-wide panel's marks (k_casc_panel: m > 2048)")
 args = ap.parse_args()
 m, n = args.m, args.n
 g = torch.Generator(device="cuda").manual_seed(0)
@@ -32,12 +34,27 @@ for rep in range(2):
     call("pdas_solve_sweeps_ws", dv.ptr(cols), dv.ptr(A), dv.ptr(d), m, n, dv.ptr(ws), rep + 1,
          dv.ptr(fail), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * 16)()
+buf = (ctypes.c_ulonglong * 32)()
 lib = load()
 lib.pdas_debug_hop_trace.argtypes = [ctypes.c_void_p]
 assert lib.pdas_debug_hop_trace(ctypes.addressof(buf)) == 0
 t = [int(v) for v in buf]
 z = t[0]
+if not args.legacy:
+    # k_casc_panel_w (warp per column): marks 0..9
+    marks = [(0, "pub: columns stored (CTA barrier)"), (1, "pub: fence + flags released"),
+             (2, "con: producer saw chunk-1 flag"), (3, "con: chunk-1 denominators staged"),
+             (9, "con: warp 0 has the first chunk-1 stage"), (4, "con: warp 0 applied all"),
+             (5, "con: triangle step 0 done"), (6, "con: chunk 0 published"),
+             (7, "con: triangle step 7 done"), (8, "con: all columns stored")]
+    print(f"m={m} n={n}: one warp-per-column panel hop (tile 15 -> 16, block 5), ns after "
+          f"the publisher's columns are stored")
+    for k, nm in marks:
+        print(f"  {nm:42s} {t[k] - z:8d}")
+    for w, b in ((0, 16), (7, 24)):
+        print(f"  tile 16 warp {w} (clock64, both reps): work {t[b]}, stage waits {t[b + 1]}, "
+              f"triangle hand-off waits {t[b + 2]}, apply steps {t[b + 3]}")
+    sys.exit(0)
 names = ["pub: triangle done", "pub: stored + fenced", "pub: flags released",
          "con: flag seen", "con: denominators staged", "con: chunk applied",
          "con: own triangle starts"]
