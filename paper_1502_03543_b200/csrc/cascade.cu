@@ -1304,6 +1304,7 @@ __device__ __forceinline__ bool panel_triangle(Tile<T, R, C, GEN>& tl, Pipe<S>& 
                 // stores -> CTA barrier -> one gpu-scope release by the producer:
                 // the barrier orders every thread's stores before the release,
                 // which is cumulative (the cooperative-groups grid-sync pattern)
+                // (deferring the release by one step: c3 unchanged, 164.2 ms)
                 tl.store(cols, col0, n + 1, cl + 1 - CH, cl + 1);
                 tl.sync();
                 if (producer) st_release(cflags + (cl + 1) / CH - 1, epoch);
@@ -1521,9 +1522,8 @@ __global__ void __launch_bounds__(T + PW, 1)
 // the end.  Breakdown and a failed earlier tile keep the stage protocol going
 // with the arithmetic skipped, so no warp waits on a stage that never comes.
 constexpr int kPwCols = 8;                        // columns per tile (CT)
-// + a producer warpgroup (one active lane) that hands its registers to the
-// column warps: 168 at launch, column warps 232, producer warpgroup 40 (the
-// 64-double column of H = 1024 does not fit 168 without spills)
+// + a producer warpgroup (one active warp): 168 registers at launch, column
+// warps 200, producer warpgroup 88 (40 spilled its flag/denominator loop)
 constexpr int kPwThreads = 32 * kPwCols + 128;
 
 __host__ __device__ inline size_t panel_w_smem(int S, int m) {
@@ -1589,7 +1589,7 @@ __global__ void __launch_bounds__(kPwThreads, 1)
     (void)hop_con;
     if (warp >= C) {
         // ---- producer warpgroup (one lane works)
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
         if (warp == C && !dead0) {
             unsigned use = 0;
             bool dead = false;
@@ -1651,7 +1651,7 @@ __global__ void __launch_bounds__(kPwThreads, 1)
         }
     } else {
         // ---- column warp: column col0 + warp of the tile
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
         const idx_t col = col0 + warp;
         const bool have = col < ncols;
         Tile<32, R, 1, false> tl;
