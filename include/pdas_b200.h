@@ -161,6 +161,10 @@ int pdas_cascade_update_tagged(double* cols, const double* a, const double* d, i
 int pdas_cascade_reset_tags(void* ws, int64_t n, void* stream);
 /* Pivots per block of the 1-GPU cascade (pdas_solve_sweeps_ws / _x0). */
 int pdas_cascade_solve_block(void);
+/* 1 when pdas_solve_sweeps_ws(_x0) runs (m, n) as the one-CTA shared-memory
+ * cascade (m <= 64, [Y|x] + A in 200 KB): no pivot-block flags, so the call
+ * is independent of the epoch and can be replayed from a CUDA graph. */
+int pdas_cascade_one_cta(int64_t m, int64_t n);
 int pdas_cascade_panel(double* cols, const double* a, const double* d, int64_t m, int64_t n,
                        int64_t q0, int64_t p0, int64_t p1, void* ws, int32_t epoch,
                        int32_t* fail_dev, void* stream);

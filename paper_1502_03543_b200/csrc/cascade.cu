@@ -2070,6 +2070,8 @@ static CascCfg cascade_cfg(idx_t m) {
 
 idx_t cascade_supported_m() { return 16384; }
 
+bool cascade_one_cta(idx_t m, idx_t n) { return small_cascade_fits(m, n); }
+
 // Side stream (high priority) + events for the panel lookahead, per device.
 struct SideStream {
     cudaStream_t ps = nullptr;  // panels (high priority)

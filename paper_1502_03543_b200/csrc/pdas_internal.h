@@ -93,6 +93,7 @@ int launch_cascade_update(double* cols, const double* a, const double* d, idx_t 
                           idx_t p0, idx_t p1, const int64_t* tiles, idx_t ntiles, double* denoms,
                           int32_t* fail_dev, cudaStream_t st, int* flags = nullptr, int utag = 0);
 idx_t cascade_supported_m();
+bool cascade_one_cta(idx_t m, idx_t n);  // the one-CTA shared-memory cascade runs (m, n)
 idx_t cascade_flags_count(idx_t m, idx_t n);
 int cascade_tile_width(idx_t m);
 idx_t cascade_profile_rows(double* out, idx_t max_rows);

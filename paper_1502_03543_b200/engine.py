@@ -17,6 +17,7 @@ PCIe bus per iteration; the SingularUpdate fallback to the direct solve
 
 from __future__ import annotations
 
+import os
 import time
 
 import numpy as np
@@ -189,6 +190,16 @@ class DeviceSolver:
         # inside the real step)
         self.time_cascade = False
         self.cascade_events = []
+        # One CUDA graph for the whole iteration (scaling, rhs, [Y|x] seed,
+        # x0 + cascade, directions, ratio test, update, objectives, state
+        # read-back) when the cascade is the one-CTA kernel: no pivot-block
+        # flags, so nothing depends on the epoch and the same graph replays
+        # every iteration.  c1 is launch-bound (~15 small launches around a
+        # 0.3 ms cascade).  PDAS_NO_GRAPH=1 keeps the eager path.
+        self._graph = None
+        self._graph_launches = 0
+        self._graph_ok = (backend == "woodbury" and not os.environ.get("PDAS_NO_GRAPH")
+                          and bool(load().pdas_cascade_one_cta(m, n)))
 
     # -- iterate I/O (host <-> device), the e2e boundary
     def load_iterate(self, x, y, s) -> None:
@@ -286,12 +297,38 @@ class DeviceSolver:
             self._solve_direct_into(self.dy_direct, self._sptr(OFF_CHOL_FAIL))
             self.dy = self.dy_direct
 
+    def _capture(self) -> None:
+        t = self.t
+        g = t.cuda.CUDAGraph()
+        side = t.cuda.Stream()
+        side.wait_stream(t.cuda.current_stream())
+        n0 = self.launches
+        with t.cuda.graph(g, stream=side):
+            self.enqueue_solve()
+            self._tail(self.dy)
+            self.state_host.copy_(self.state, non_blocking=True)
+        t.cuda.current_stream().wait_stream(side)
+        self._graph_launches = self.launches - n0
+        self.launches = n0
+        self._graph = g
+
+    def _solve_and_fetch(self) -> PdasIterState:
+        if self._graph_ok and not self.time_cascade:
+            if self._graph is None:
+                self._capture()
+            self._graph.replay()
+            self.launches += self._graph_launches
+            self.dy = self.xcol
+            dv.synchronize()
+            return PdasIterState.from_buffer_copy(self.state_host.numpy().tobytes())
+        self.enqueue_solve()
+        self._tail(self.dy)
+        return self._fetch_state()
+
     def iterate(self) -> IterResult:
         """One PDAS iteration on device; returns the host copy of its state."""
         t0 = time.perf_counter()
-        self.enqueue_solve()
-        self._tail(self.dy)
-        st = self._fetch_state()
+        st = self._solve_and_fetch()
         if self.backend == "woodbury" and st.cascade_fail != 0 and not not_interior(
                 st.interior_flags):
             # SingularUpdate -> retry with the direct solve, flagged (solver.py:161-165)

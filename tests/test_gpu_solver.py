@@ -47,6 +47,27 @@ def test_c1_trajectory_bitwise(gpu, seed):
     assert bits_equal(p.x, g["x"]) and bits_equal(p.y, g["y"]) and bits_equal(p.s, g["s"])
 
 
+def test_c1_graph_replay_matches_eager(gpu, monkeypatch):
+    """The one-CTA cascade's iteration is replayed from one CUDA graph
+    (engine.DeviceSolver._capture); the eager launches give the same bits."""
+    from paper_1502_03543_b200.engine import DeviceProblem, DeviceSolver
+
+    P = gpu
+    lp, start = P.gen_random_feasible(50, 200, 3)
+    runs = []
+    for no_graph in (False, True):
+        if no_graph:
+            monkeypatch.setenv("PDAS_NO_GRAPH", "1")
+        prob = DeviceProblem.from_lp(lp)
+        eng = DeviceSolver(prob, L0=prob.validate())
+        assert eng._graph_ok == (not no_graph)
+        eng.load_iterate(start.x, start.y, start.s)
+        states = [bytes(eng.iterate().state) for _ in range(4)]
+        assert (eng._graph is not None) == (not no_graph)
+        runs.append((states, [sha(v) for v in eng.read_iterate()]))
+    assert runs[0] == runs[1]
+
+
 def test_c1_basis_and_first_iteration(gpu):
     P = gpu
     g = load_golden("c1_seed0.npz")
