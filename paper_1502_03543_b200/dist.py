@@ -525,6 +525,8 @@ class ShardedSolver(DeviceSolver):
     kernels, same bits), so the only traffic is the cascade's block
     broadcasts plus one x-column broadcast per iteration."""
 
+    graph_iterations = False  # collectives and the per-rank schedule: eager
+
     def __init__(self, prob, group=None, rho: float = 0.9, basis=None, L0=None,
                  block: Optional[int] = None, exchange: str = "nccl"):
         """exchange: "nccl" (a broadcast per block) or "peer" (the fused

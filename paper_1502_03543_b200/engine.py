@@ -156,6 +156,10 @@ class IterResult:
 class DeviceSolver:
     """Device-resident PDAS iteration for one LP (see module docstring)."""
 
+    # subclasses whose iteration is not one replayable launch sequence (the
+    # sharded solver: collectives, per-rank schedule) turn the graph off
+    graph_iterations = True
+
     def __init__(self, prob: DeviceProblem, backend: str = "woodbury", rho: float = 0.9,
                  basis: DeviceBasis = None, L0=None):
         t = dv.require_gpu()
@@ -198,7 +202,8 @@ class DeviceSolver:
         # 0.3 ms cascade).  PDAS_NO_GRAPH=1 keeps the eager path.
         self._graph = None
         self._graph_launches = 0
-        self._graph_ok = (backend == "woodbury" and not os.environ.get("PDAS_NO_GRAPH")
+        self._graph_ok = (self.graph_iterations and backend == "woodbury"
+                          and not os.environ.get("PDAS_NO_GRAPH")
                           and bool(load().pdas_cascade_one_cta(m, n)))
 
     # -- iterate I/O (host <-> device), the e2e boundary

@@ -1,8 +1,16 @@
-import ctypes, sys, os
-sys.path.insert(0, "/root/repo")
-import torch
-from paper_1502_03543_b200 import _device as dv
-from paper_1502_03543_b200._lib import call, load
+"""The warp-specialized update kernel alone (pdas_cascade_update: one tile per
+CTA, 128 pivots) on 148 / 296 / 1480 tiles at m = 2048 and 2000, in cycles per
+tile-pivot per wave -- compare with the micro's steady state
+(tools/micro/ws2.cu).  profiles/r02_update_isolated.txt.
+
+    python tools/update_isolated.py"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+from paper_1502_03543_b200 import _device as dv  # noqa: E402
+from paper_1502_03543_b200._lib import call, load  # noqa: E402
 m, n = 2048, 8 * 2000
 for m in (2048, 2000):
     g = torch.Generator(device="cuda").manual_seed(0)
