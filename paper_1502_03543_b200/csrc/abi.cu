@@ -362,7 +362,8 @@ int pdas_cascade_reset_tags(void* ws, int64_t n, void* stream) {
     int* flags;
     split_ws(ws, n, &denoms, &flags);
     return check_cuda(
-        cudaMemsetAsync(flags + (n + 2), 0, sizeof(int) * (size_t)(n + 2), S(stream)) == cudaSuccess
+        cudaMemsetAsync(flags + pdas::panel_flag_ints(n), 0,
+                        sizeof(int) * (size_t)pdas::panel_flag_ints(n), S(stream)) == cudaSuccess
             ? PDAS_OK
             : PDAS_ERR_CUDA,
         "cascade_reset_tags");

@@ -1525,11 +1525,17 @@ constexpr int kPwCols = 8;                        // columns per tile (CT)
 // + a producer warpgroup (one active warp): 168 registers at launch, column
 // warps 200, producer warpgroup 88 (40 spilled its flag/denominator loop)
 constexpr int kPwThreads = 32 * kPwCols + 128;
+// its final columns go out in kPwChunks chunks of two (flags[tile * kPwChunks +
+// ch]): a column warp that has finished its own step has nothing left but stage
+// bookkeeping, so finer publication costs the working warps nothing (2 chunks:
+// c2 10.5 ms, 4: 9.8, 8: 10.9 -- a flag per pivot is more consumer overhead)
+constexpr int kPwChunks = 4;
+static_assert(kPwCols % kPwChunks == 0, "chunks");
 
 __host__ __device__ inline size_t panel_w_smem(int S, int m) {
     const size_t mp = (size_t)((m + 1) & ~1);
     return (size_t)S * 2 * mp * 8 + 3 * (size_t)kMaxBlock * 8 + kPwCols * 8 + kPwCols * 4 +
-           (2 * (size_t)S + kPwCols) * 8 + 16;
+           (2 * (size_t)S + kPwCols) * 8 + 4 * (1 + kPwChunks) + 16;
 }
 
 template <int R, int S, bool FULL>
@@ -1538,7 +1544,7 @@ __global__ void __launch_bounds__(kPwThreads, 1)
                    const double* __restrict__ d, double* __restrict__ denoms, int m, idx_t n,
                    idx_t p0, idx_t p1, int32_t* __restrict__ fail, int* __restrict__ flags,
                    int epoch, const int* __restrict__ uflag, int utag) {
-    constexpr int C = kPwCols, CH = C / kPanelChunks, NCH = kPanelChunks;
+    constexpr int C = kPwCols, NCH = kPwChunks, CH = C / NCH;
     const idx_t tile = p0 / C + blockIdx.x;
     if (__syncthreads_or(threadIdx.x == 0 && *(volatile int32_t*)fail != 0)) {
         if (threadIdx.x == 0)
@@ -1556,7 +1562,7 @@ __global__ void __launch_bounds__(kPwThreads, 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(stbrk + C);
     uint64_t* empty = full + S;
     uint64_t* tri = empty + S;
-    int* s_state = reinterpret_cast<int*>(tri + C);      // [0] dead, [1] chunk-0 count
+    int* s_state = reinterpret_cast<int*>(tri + C);      // [0] dead, [1 + ch] chunk counts
     const uint32_t full_a = smem_addr(full), empty_a = smem_addr(empty), tri_a = smem_addr(tri);
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
@@ -1564,8 +1570,7 @@ __global__ void __launch_bounds__(kPwThreads, 1)
             mbar_init(empty + s, C);
         }
         for (int k = 0; k < C; ++k) mbar_init(tri + k, 1);
-        s_state[0] = 0;
-        s_state[1] = 0;
+        for (int k = 0; k <= NCH; ++k) s_state[k] = 0;
         mbar_fence_init();
     }
     for (idx_t l = p0 + threadIdx.x; l < p1; l += blockDim.x) sd[l - p0] = __ldg(d + l);
@@ -1735,7 +1740,8 @@ __global__ void __launch_bounds__(kPwThreads, 1)
 #endif
             PW_MARK(hop_con && warp == 0 && lane == 0, 4);
             // the triangle over the tile's own pivots
-            const bool mid = cnt > CH;  // chunk 0 goes out before the triangle ends
+            const int wch = warp / CH;  // this column's chunk, out before the triangle
+            const bool mid = (wch + 1) * CH < cnt;  // ends iff it ends before the last pivot
             for (int cl = 0; cl < cnt; ++cl) {
                 const idx_t l = col0 + cl;
                 const double dl = sd[l - p0];
@@ -1778,7 +1784,7 @@ __global__ void __launch_bounds__(kPwThreads, 1)
                 }
                 release_stage(sl);
                 }
-                if (cl == warp && mid && warp < CH && !dead && !broken) {
+                if (cl == warp && mid && !dead && !broken) {
                     // column and denominator final: store the column; the last
                     // of the chunk's warps releases the chunk flag (shared
                     // count, then one cumulative gpu-scope fence)
@@ -1786,10 +1792,10 @@ __global__ void __launch_bounds__(kPwThreads, 1)
                     __syncwarp();
                     if (lane == 0) {
                         __threadfence_block();
-                        if (atomicAdd(s_state + 1, 1) == CH - 1) {
+                        if (atomicAdd(s_state + 1 + wch, 1) == CH - 1) {
                             __threadfence();
-                            st_relaxed(flags + tile * NCH, epoch);
-                            PW_MARK(hop_con, 6);
+                            st_relaxed(flags + tile * NCH + wch, epoch);
+                            PW_MARK(hop_con && wch == 0, 6);
                         }
                     }
                     stored = true;
@@ -2287,8 +2293,8 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         // tile as it lands; panel(b+1) -- only the block's own chain and
         // triangle -- waits on those flags inside the kernel, so it starts as
         // soon as its 16-odd tiles are done instead of after all of U(b).
-        int* uflag = flags + (n + 2);
-        cudaMemsetAsync(uflag, 0, sizeof(int) * (size_t)(n + 2), st);
+        int* uflag = flags + panel_flag_ints(n);
+        cudaMemsetAsync(uflag, 0, sizeof(int) * (size_t)panel_flag_ints(n), st);
         CascProfile prof(2 * nb + 1, st);
         // x lane: column n alone in the last tile -> the x0 solve and that
         // tile's updates run on their own stream, off the Y critical path
@@ -2328,7 +2334,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         // their start).  Ordering then comes from flags, not from the stream:
         // each CTA waits for panel(b)'s last chunk flag and for its tile's
         // U(b-1) (tile_done = uflag[tile] >= b, set by every update CTA).
-        const int nch = panel_flag_chunks(CT);
+        const int nch = pw ? kPwChunks : panel_flag_chunks(CT);
         auto upd = [&](cudaStream_t s_, idx_t b, idx_t ta, idx_t tb, int* uf) {
             if (ta >= tb) return;
             const bool chained = b > 0;
@@ -2432,7 +2438,7 @@ static int run_cascade(double* cols, const double* a, const double* d, int m, id
                                                        epoch, B, st, op);
 }
 
-idx_t cascade_flags_count(idx_t m, idx_t n) { return 2 * (n + 2); }  // panel + update flags
+idx_t cascade_flags_count(idx_t m, idx_t n) { return 2 * panel_flag_ints(n); }  // panel + update
 
 #if PDAS_PANEL_TRACE
 }  // namespace pdas
@@ -2525,7 +2531,7 @@ int launch_cascade_panel(double* cols, const double* a, const double* d, idx_t m
     op.p0 = p0;
     op.p1 = p1;
     if (utag > 0) {  // chained: wait for this rank's own update of the tiles
-        op.uflag = flags + (n + 2);
+        op.uflag = flags + panel_flag_ints(n);
         op.utag = utag;
     }
     if (peers) {
@@ -2579,7 +2585,7 @@ int launch_cascade_update(double* cols, const double* a, const double* d, idx_t 
     op.tiles = tiles;
     op.ntiles = ntiles;
     if (flags && utag > 0) {  // publish tile_done = utag for every tile updated
-        op.uflag = flags + (n + 2);
+        op.uflag = flags + panel_flag_ints(n);
         op.utag = utag;
     }
     return dispatch_cascade(cols, a, d, m, n, denoms, fail_dev, nullptr, 0, kMaxBlock, st, op);

@@ -95,6 +95,9 @@ int launch_cascade_update(double* cols, const double* a, const double* d, idx_t 
 idx_t cascade_supported_m();
 bool cascade_one_cta(idx_t m, idx_t n);  // the one-CTA shared-memory cascade runs (m, n)
 idx_t cascade_flags_count(idx_t m, idx_t n);
+// the workspace's int flags: [0, panel_flag_ints(n)) panel chunk flags (up to
+// 8 per 8-column tile), then as many update tile tags (cascade_flags_count = 2x)
+inline idx_t panel_flag_ints(idx_t n) { return n + 16; }
 int cascade_tile_width(idx_t m);
 idx_t cascade_profile_rows(double* out, idx_t max_rows);
 // Pivot blocks (B, pivots per panel/update round): the 1-GPU cascade uses
