@@ -2265,9 +2265,15 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
     const idx_t ntiles = (n + 1 + CT - 1) / CT;
     if (op.kind == 1) {
         if (op.p0 % CT || op.p1 <= op.p0 || op.p1 - op.q0 > 2 * kMaxBlock) return PDAS_ERR_ARG;
-        kp<<<(unsigned)((op.p1 - op.p0 + CT - 1) / CT), TPB, smem_p, st>>>(
-            cols, a, d, denoms, m, n, op.q0, op.p0, op.p1, fail, flags, epoch, op.uflag, op.utag,
-            op.peers);
+        // a chained block of the NCCL-exchange schedule: nothing outside this
+        // launch reads its chunk flags (the fused exchange's k_peer_wait reads
+        // them in the CTA-wide panel's layout, so it keeps that panel)
+        if (op.q0 == op.p0 && op.peers.count == 0 && op.uflag != nullptr)
+            panel(st, op.p0, op.p1, op.uflag, op.utag);
+        else
+            kp<<<(unsigned)((op.p1 - op.p0 + CT - 1) / CT), TPB, smem_p, st>>>(
+                cols, a, d, denoms, m, n, op.q0, op.p0, op.p1, fail, flags, epoch, op.uflag,
+                op.utag, op.peers);
         return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
     }
     if (op.kind == 2) {
