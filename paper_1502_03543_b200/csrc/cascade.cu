@@ -1104,7 +1104,26 @@ __global__ void __launch_bounds__(TC + 128, TC == 128 ? 2 : 1)
     const idx_t tile = tiles ? tiles[blockIdx.x] : tile0 + blockIdx.x;
     update_deps(pflag, epoch, uflag, tile, need, fail);
     __syncthreads();
-    stage_scalars(pp, d, denoms, p0, p0, p1, true);
+    // TC = 256 (168 registers at launch hold the 64-double tile): the compute
+    // threads' tile loads go out first and the reducer warpgroup stages the
+    // pivot scalars while they are in flight.  TC = 128 (128 at launch) loads
+    // the tile after setmaxnreg.
+    constexpr bool kEarly = TC == 256;
+    Tile<TC, R, C, false> tl;
+    const idx_t col0 = tile * C;
+    if (kEarly && threadIdx.x < TC) {
+        tl.init(threadIdx.x, m, 0, red, bc);
+        tl.load(cols, col0, n + 1);
+    } else if (kEarly) {
+        for (idx_t l = p0 + (threadIdx.x - TC); l < p1; l += blockDim.x - TC) {
+            pp.sd[l - p0] = __ldg(d + l);
+            const double den = __ldcg(denoms + l);
+            pp.sden[l - p0] = den;
+            pp.sy[l - p0] = div_recip(den);
+        }
+    } else {
+        stage_scalars(pp, d, denoms, p0, p0, p1, true);
+    }
     // a breakdown found by a concurrent panel: one thread reads the fail word and
     // the whole CTA leaves together (before setmaxnreg and the barrier protocol)
     if (__syncthreads_or(threadIdx.x == 0 && *(volatile const int32_t*)fail != 0)) return;
@@ -1123,10 +1142,10 @@ __global__ void __launch_bounds__(TC + 128, TC == 128 ? 2 : 1)
         return;
     }
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegC));
-    Tile<TC, R, C, false> tl;
-    tl.init(threadIdx.x, m, 0, red, bc);
-    const idx_t col0 = tile * C;
-    tl.load(cols, col0, n + 1);
+    if (!kEarly) {
+        tl.init(threadIdx.x, m, 0, red, bc);
+        tl.load(cols, col0, n + 1);
+    }
     const bool full = __all_sync(0xffffffffu, tl.full());
     if constexpr (kLdg) {
         const double* pc = cols + p0 * m;
