@@ -2309,9 +2309,23 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         }
         return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
     }
-    const idx_t nb = (n + B - 1) / B;
-    auto blk_end = [&](idx_t b) { return (b + 1) * B < n ? (b + 1) * B : n; };
-    auto tiles_of = [&](idx_t b) { return (blk_end(b) - b * B + CT - 1) / CT; };
+    // pivot blocks: the first one B (its panel runs alone), the others 2B for
+    // the one-CTA-per-SM layouts: half the update CTAs and their start-up
+    // (c3 161.5 -> 160.8 ms; 2B only over the first half of n: 161.0).  The
+    // warp-per-column panel's scalar window holds B pivots.
+    std::vector<idx_t> bst{0};
+    {
+        const idx_t big = !pw && 2 * B <= 2 * kMaxBlock ? 2 * B : B;
+        while (bst.back() < n) {
+            const idx_t at = bst.back();
+            const idx_t len = at > 0 ? big : B;
+            bst.push_back(at + len < n ? at + len : n);
+        }
+    }
+    const idx_t nb = (idx_t)bst.size() - 1;
+    auto bs = [&](idx_t b) { return bst[(size_t)b]; };
+    auto blk_end = [&](idx_t b) { return bst[(size_t)b + 1]; };
+    auto tiles_of = [&](idx_t b) { return (blk_end(b) - bs(b) + CT - 1) / CT; };
     SideStream& ss = side_stream();
     {
         // U(b) covers block b+1's tiles too (its lowest CTAs) and flags each
@@ -2327,11 +2341,11 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         const idx_t nt_y = xlane ? ntiles - 1 : ntiles;  // tiles U(b) covers
         auto update_x = [&](idx_t b) {  // block b -> the x tile (1 CTA)
             if (use_ws)
-                kws<<<1, ws_threads, smem_ws, ss.xs>>>(cols, a, d, denoms, m, n, b * B, blk_end(b),
+                kws<<<1, ws_threads, smem_ws, ss.xs>>>(cols, a, d, denoms, m, n, bs(b), blk_end(b),
                                                        ntiles - 1, fail, nullptr, nullptr, 0, 0,
                                                        nullptr, 0);
             else
-                ku<<<1, T * G, smem_u, ss.xs>>>(cols, a, d, denoms, m, n, b * B, blk_end(b),
+                ku<<<1, T * G, smem_u, ss.xs>>>(cols, a, d, denoms, m, n, bs(b), blk_end(b),
                                                 ntiles - 1, fail, nullptr, nullptr, 0, 0, nullptr,
                                                 0);
         };
@@ -2363,7 +2377,7 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         auto upd = [&](cudaStream_t s_, idx_t b, idx_t ta, idx_t tb, int* uf) {
             if (ta >= tb) return;
             const bool chained = b > 0;
-            const int* pflag = chained ? flags + (b * B / CT + tiles_of(b) - 1) * nch + nch - 1
+            const int* pflag = chained ? flags + (bs(b) / CT + tiles_of(b) - 1) * nch + nch - 1
                                        : nullptr;
             const int need = chained ? (int)b : 0;
             cudaLaunchConfig_t lc = {};
@@ -2381,12 +2395,12 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
             if (use_ws) {
                 lc.blockDim = dim3(ws_threads);
                 lc.dynamicSmemBytes = smem_ws;
-                cudaLaunchKernelEx(&lc, kws, cols, a, dd, dn, m, n, b * B, blk_end(b), ta,
+                cudaLaunchKernelEx(&lc, kws, cols, a, dd, dn, m, n, bs(b), blk_end(b), ta,
                                    (const int32_t*)fail, no_tiles, uf, utag, need, pflag, epoch);
             } else {
                 lc.blockDim = dim3(T * G);
                 lc.dynamicSmemBytes = smem_u;
-                cudaLaunchKernelEx(&lc, ku, cols, a, dd, dn, m, n, b * B, blk_end(b), ta,
+                cudaLaunchKernelEx(&lc, ku, cols, a, dd, dn, m, n, bs(b), blk_end(b), ta,
                                    (const int32_t*)fail, no_tiles, uf, utag, need, pflag, epoch);
             }
         };
@@ -2400,12 +2414,12 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
             // eU: the main stream up to U(b-1); panel(b+1) must not be resident
             // (spinning on its SMs) while U(b-1) still runs
             cudaEventRecord(ss.eU, st);
-            const idx_t t0 = b + 1 < nb ? (b + 1) * B / CT : (n + CT - 1) / CT;
+            const idx_t t0 = b + 1 < nb ? bs(b + 1) / CT : (n + CT - 1) / CT;
             prof.mark(st, 0, b, 0);
             upd(st, b, t0, nt_y, uflag);
             prof.mark(st, 0, b, 1);
             if (b + 1 < nb) {
-                const idx_t p0 = (b + 1) * B;
+                const idx_t p0 = bs(b + 1);
                 cudaStreamWaitEvent(ss.ps, ss.eU, 0);
                 prof.mark(ss.ps, 1, b + 1, 0);
                 panel(ss.ps, p0, blk_end(b + 1), uflag, (int)(b + 1));
