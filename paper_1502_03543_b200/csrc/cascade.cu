@@ -1553,7 +1553,7 @@ static_assert(kPwCols % kPwChunks == 0, "chunks");
 
 __host__ __device__ inline size_t panel_w_smem(int S, int m) {
     const size_t mp = (size_t)((m + 1) & ~1);
-    return (size_t)S * 2 * mp * 8 + 3 * (size_t)kMaxBlock * 8 + kPwCols * 8 + kPwCols * 4 +
+    return (size_t)S * 2 * mp * 8 + 6 * (size_t)kMaxBlock * 8 + kPwCols * 8 + kPwCols * 4 +
            (2 * (size_t)S + kPwCols) * 8 + 4 * (1 + kPwChunks) + 16;
 }
 
@@ -1574,9 +1574,9 @@ __global__ void __launch_bounds__(kPwThreads, 1)
     const int mp = (m + 1) & ~1;
     double* buf = reinterpret_cast<double*>(smem_raw);  // S x [P | A]
     double* sd = buf + (size_t)S * 2 * mp;               // d, window base p0
-    double* sden = sd + kMaxBlock;                       // earlier tiles' denominators
-    double* sy = sden + kMaxBlock;                       // and their div_recip
-    double* stden = sy + kMaxBlock;                      // this tile's denominators
+    double* sden = sd + 2 * kMaxBlock;                   // earlier tiles' denominators
+    double* sy = sden + 2 * kMaxBlock;                   // and their div_recip
+    double* stden = sy + 2 * kMaxBlock;                  // this tile's denominators
     int* stbrk = reinterpret_cast<int*>(stden + C);      // step cl broke down
     uint64_t* full = reinterpret_cast<uint64_t*>(stbrk + C);
     uint64_t* empty = full + S;
@@ -2309,13 +2309,12 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         }
         return cudaGetLastError() == cudaSuccess ? PDAS_OK : PDAS_ERR_CUDA;
     }
-    // pivot blocks: the first one B (its panel runs alone), the others 2B for
-    // the one-CTA-per-SM layouts: half the update CTAs and their start-up
-    // (c3 161.5 -> 160.8 ms; 2B only over the first half of n: 161.0).  The
-    // warp-per-column panel's scalar window holds B pivots.
+    // pivot blocks: the first one B (its panel runs alone), the others 2B:
+    // half the update CTAs, their start-up and tile reloads (c3 161.5 -> 160.8
+    // ms, c4 1929 -> 1915; 2B only over the first half of n: c3 161.0)
     std::vector<idx_t> bst{0};
     {
-        const idx_t big = !pw && 2 * B <= 2 * kMaxBlock ? 2 * B : B;
+        const idx_t big = 2 * B <= 2 * kMaxBlock ? 2 * B : B;
         while (bst.back() < n) {
             const idx_t at = bst.back();
             const idx_t len = at > 0 ? big : B;
