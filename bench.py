@@ -102,7 +102,9 @@ class ClockSampler:
 def cascade_traffic(n, block=256):
     """DRAM bytes (read + write) of one c3 cascade, from the committed ncu
     launch list of `tools/cascade_time.py` (profiles/r02_launches_cascade.json:
-    per-kernel sums of dram__bytes_read.sum + dram__bytes_write.sum)."""
+    per-kernel sums of dram__bytes_read.sum + dram__bytes_write.sum).  One
+    panel launch per pivot block: the first block has `block` pivots, the
+    others 2 * block (cascade.cu run_cascade_impl)."""
     try:
         d = json.load(open(os.path.join(REPO, "profiles", "r02_launches_cascade.json")))
     except Exception:
@@ -111,7 +113,8 @@ def cascade_traffic(n, block=256):
     panels = sum(v["launches"] for k, v in casc.items() if "panel" in k)
     if not panels:
         return None
-    ncasc = panels / ((n + block - 1) // block)
+    blocks = 1 + max(0, (n - block + 2 * block - 1) // (2 * block))
+    ncasc = panels / blocks
     return sum(v["dram_bytes"] for v in casc.values()) / ncasc
 
 
