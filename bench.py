@@ -375,7 +375,8 @@ def run_ours(args):
                         f"{args.exchange} block exchange)" if shard
                         else f"replicas x{world}" if world > 1 else "1 GPU"),
         "cascade_block_pivots": (int(load_lib().pdas_cascade_block_pivots()) if shard
-                                 else int(load_lib().pdas_cascade_solve_block())),
+                                 else f"{int(load_lib().pdas_cascade_solve_block())} then "
+                                      f"{2 * int(load_lib().pdas_cascade_solve_block())}"),
         "e2e": {"value": jobs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,

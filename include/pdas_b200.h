@@ -159,8 +159,12 @@ int pdas_cascade_update_tagged(double* cols, const double* a, const double* d, i
                                int64_t ntiles, void* ws, int32_t* fail_dev, int32_t utag,
                                void* stream);
 int pdas_cascade_reset_tags(void* ws, int64_t n, void* stream);
-/* Pivots per block of the 1-GPU cascade (pdas_solve_sweeps_ws / _x0). */
+/* Pivots in the first block of the 1-GPU cascade (pdas_solve_sweeps_ws / _x0);
+ * the later blocks have twice as many. */
 int pdas_cascade_solve_block(void);
+/* Pivot blocks (panel + update launches each) of the 1-GPU cascade of (m, n);
+ * 0 for the one-CTA cascade (a single kernel). */
+int64_t pdas_cascade_solve_blocks(int64_t m, int64_t n);
 /* 1 when pdas_solve_sweeps_ws(_x0) runs (m, n) as the one-CTA shared-memory
  * cascade (m <= 64, [Y|x] + A in 200 KB): no pivot-block flags, so the call
  * is independent of the epoch and can be replayed from a CUDA graph. */

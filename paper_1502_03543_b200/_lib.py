@@ -78,6 +78,7 @@ SIGNATURES = {
     "pdas_cascade_block_pivots": (ctypes.c_int, []),
     "pdas_cascade_solve_block": (ctypes.c_int, []),
     "pdas_cascade_one_cta": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64]),
+    "pdas_cascade_solve_blocks": (ctypes.c_int64, [ctypes.c_int64, ctypes.c_int64]),
     "pdas_cascade_panel": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, _I64, _I64, _I64, _VP,
                                           ctypes.c_int32, _VP, _VP]),
     "pdas_cascade_update": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, _I64, _I64, _VP, _I64,

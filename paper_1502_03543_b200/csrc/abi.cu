@@ -221,6 +221,10 @@ int pdas_cascade_tile_width(int64_t m) {
 int pdas_cascade_block_pivots(void) { return pdas::kShardBlock; }
 int pdas_cascade_solve_block(void) { return pdas::kSolveBlock; }
 int pdas_cascade_one_cta(int64_t m, int64_t n) { return pdas::cascade_one_cta(m, n) ? 1 : 0; }
+int64_t pdas_cascade_solve_blocks(int64_t m, int64_t n) {
+    if (m < 1 || n < 1 || pdas::cascade_one_cta(m, n)) return 0;
+    return pdas::cascade_solve_blocks(n);
+}
 
 int64_t pdas_debug_cascade_profile(double* out, int64_t max_rows) {
     if (max_rows < 0 || (max_rows > 0 && out == nullptr)) return -1;

@@ -94,6 +94,7 @@ int launch_cascade_update(double* cols, const double* a, const double* d, idx_t 
                           int32_t* fail_dev, cudaStream_t st, int* flags = nullptr, int utag = 0);
 idx_t cascade_supported_m();
 bool cascade_one_cta(idx_t m, idx_t n);  // the one-CTA shared-memory cascade runs (m, n)
+
 idx_t cascade_flags_count(idx_t m, idx_t n);
 // the workspace's int flags: [0, panel_flag_ints(n)) panel chunk flags (up to
 // 8 per 8-column tile), then as many update tile tags (cascade_flags_count = 2x)
@@ -108,6 +109,11 @@ constexpr int kMaxBlock = 256;
 constexpr int kSolveBlock = 256;  // c3: 2 % faster than 128 (per-tile reload, launches)
 constexpr int kShardBlock = 128;
 static_assert(kSolveBlock <= kMaxBlock && 2 * kShardBlock <= 2 * kMaxBlock, "block sizes");
+// pivot blocks of the 1-GPU cascade (run_cascade_impl): kSolveBlock, then
+// 2 * kSolveBlock each
+inline idx_t cascade_solve_blocks(idx_t n) {
+    return n <= kSolveBlock ? 1 : 1 + (n - kSolveBlock + 2 * kSolveBlock - 1) / (2 * kSolveBlock);
+}
 
 // solve_kernels.cu (single right-hand side, latency-optimised)
 int launch_solve_one(const double* low, idx_t m, double* x, double* work, cudaStream_t st);

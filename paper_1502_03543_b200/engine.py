@@ -272,10 +272,11 @@ class DeviceSolver:
         call("pdas_solve_sweeps_ws_x0", dv.ptr(self.cols), dv.ptr(self.prob.A), dv.ptr(self.d),
              dv.ptr(self.basis.L0), m, n, dv.ptr(self.casc_ws), self.epoch,
              self._sptr(OFF_CASCADE_FAIL), dv.stream())
-        # x0 solve (2) + per pivot block: panel, update, and the x lane's update
-        blk = int(load().pdas_cascade_solve_block())
+        # one-CTA cascade: one kernel (x0 inside); else x0 solve (2) + per pivot
+        # block: panel, update, and the x lane's update
+        nb = int(load().pdas_cascade_solve_blocks(m, n))
         xlane = n % int(load().pdas_cascade_tile_width(m)) == 0
-        self.launches += 2 + (3 if xlane else 2) * ((n + blk - 1) // blk)
+        self.launches += 1 if nb == 0 else 2 + (3 if xlane else 2) * nb
 
     def enqueue_solve(self) -> None:
         """Scaling, rhs and the normal-equations solve (cascade or direct)."""
