@@ -309,19 +309,25 @@ class DeviceSolver:
         side = t.cuda.Stream()
         side.wait_stream(t.cuda.current_stream())
         n0 = self.launches
-        with t.cuda.graph(g, stream=side):
-            self.enqueue_solve()
-            self._tail(self.dy)
-            self.state_host.copy_(self.state, non_blocking=True)
-        t.cuda.current_stream().wait_stream(side)
-        self._graph_launches = self.launches - n0
-        self.launches = n0
+        try:
+            with t.cuda.graph(g, stream=side):
+                self.enqueue_solve()
+                self._tail(self.dy)
+                self.state_host.copy_(self.state, non_blocking=True)
+        finally:
+            t.cuda.current_stream().wait_stream(side)
+            self._graph_launches = self.launches - n0
+            self.launches = n0
         self._graph = g
 
     def _solve_and_fetch(self) -> PdasIterState:
-        if self._graph_ok and not self.time_cascade:
-            if self._graph is None:
+        if self._graph_ok and not self.time_cascade and self._graph is None:
+            try:
                 self._capture()
+            except RuntimeError:  # capture refused (driver/runtime): eager launches
+                self._graph_ok = False
+                self.t.cuda.synchronize()
+        if self._graph_ok and not self.time_cascade:
             self._graph.replay()
             self.launches += self._graph_launches
             self.dy = self.xcol
