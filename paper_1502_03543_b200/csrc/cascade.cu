@@ -1352,17 +1352,21 @@ __global__ void __launch_bounds__(T + PW, 1)
                  const double* __restrict__ d, double* __restrict__ denoms, int m, idx_t n,
                  idx_t q0, idx_t p0, idx_t p1, int32_t* __restrict__ fail, int* __restrict__ flags,
                  int epoch, const int* __restrict__ uflag, int utag, const PeerSet peers) {
-    const idx_t tile = p0 / C + blockIdx.x;
+    // tiles of the block: CTA j takes j, j + G, ... (G = gridDim.x < tiles when
+    // the host gives a CTA two tiles: the second one's catch-up fits in the
+    // chain's slack, and the panel holds half the SMs)
+    const idx_t tile_beg = p0 / C, tile_end = (p1 + C - 1) / C;
     // a tile's final columns are published in NCH chunks of CH (flags[tile*NCH + ch])
     constexpr int CH = C / kPanelChunks > 0 ? C / kPanelChunks : 1;
     constexpr int NCH = C / CH;
     // block-uniform: thread 0 reads the fail word for the whole CTA
     if (__syncthreads_or(threadIdx.x == 0 && *(volatile int32_t*)fail != 0)) {
         // still publish: later tiles may be waiting
-        if (threadIdx.x == 0) {
-            for (int ch = 0; ch < NCH; ++ch) st_release(flags + tile * NCH + ch, epoch);
-            peer_signal(peers, fail, flags, tile * NCH + NCH - 1, epoch);
-        }
+        if (threadIdx.x == 0)
+            for (idx_t tile = tile_beg + blockIdx.x; tile < tile_end; tile += gridDim.x) {
+                for (int ch = 0; ch < NCH; ++ch) st_release(flags + tile * NCH + ch, epoch);
+                peer_signal(peers, fail, flags, tile * NCH + NCH - 1, epoch);
+            }
         return;
     }
     double *red, *bc;
@@ -1374,6 +1378,7 @@ __global__ void __launch_bounds__(T + PW, 1)
     __syncthreads();
     const bool pubw = PW > 0 && (int)threadIdx.x >= T;  // the publisher warp
     __shared__ int s_pub;
+    for (idx_t tile = tile_beg + blockIdx.x; tile < tile_end; tile += gridDim.x) {
     Tile<T, R, C, GEN> tl;
     tl.init(pubw ? 0 : (int)threadIdx.x, m, 1, red, bc);
     const bool producer = threadIdx.x == 0;
@@ -1521,6 +1526,8 @@ __global__ void __launch_bounds__(T + PW, 1)
         for (int ch = 0; ch < NCH; ++ch) st_relaxed(flags + tile * NCH + ch, epoch);
     }
     HOP_MARK(hop_pub, 2);
+    __syncthreads();  // shared reduction rows and scalars reused by the next tile
+    }
 }
 
 // ------------------------------------------------------------ warp-per-column panel
@@ -2277,9 +2284,9 @@ static int run_cascade_impl(double* cols, const double* a, const double* d, int 
         if (pw)
             kpw<<<nt_, kPwThreads, smem_w, s_>>>(cols, a, d, denoms, m, n, p0_, p1_, fail, flags,
                                                  epoch, uf, ut);
-        else
-            kp<<<nt_, TPB, smem_p, s_>>>(cols, a, d, denoms, m, n, p0_, p0_, p1_, fail, flags,
-                                         epoch, uf, ut, PeerSet{});
+        else  // more than 32 tiles (512-pivot blocks): two tiles per CTA
+            kp<<<nt_ > 32 ? (nt_ + 1) / 2 : nt_, TPB, smem_p, s_>>>(
+                cols, a, d, denoms, m, n, p0_, p0_, p1_, fail, flags, epoch, uf, ut, PeerSet{});
     };
     const idx_t ntiles = (n + 1 + CT - 1) / CT;
     if (op.kind == 1) {
