@@ -1531,7 +1531,7 @@ __global__ void __launch_bounds__(T + PW, 1)
 }
 
 // ------------------------------------------------------------ warp-per-column panel
-// The panel as a latency chain of 8-column tiles (c2, c3, c5: 64 <= H <= 1024,
+// The panel as a latency chain of 8-column tiles (c2, c4, c5: 64 <= H <= 512;
 // one pivot block, nothing of the previous block left to apply).  Each of the
 // tile's columns lives in ONE warp (Tile<32, H/32, 1>: rows lane + 32 r and
 // + H, the same reference tree: in-lane levels, then the 32-lane butterfly),
@@ -1543,9 +1543,10 @@ __global__ void __launch_bounds__(T + PW, 1)
 // empty: one arrival per column warp).  Triangle step cl: warp cl writes its
 // final column into the stage's P half, reduces its own denominator and
 // releases tri[cl]; warps c > cl reduce their columns meanwhile and apply the
-// step after tri[cl].  Chunk 0 (columns 0..3) is published by the last of its
-// four warps to finish (shared-memory count, one gpu-scope fence), the rest at
-// the end.  Breakdown and a failed earlier tile keep the stage protocol going
+// step after tri[cl].  A chunk of columns that ends before the tile's last
+// pivot is published by the last of its warps to finish (shared-memory count,
+// one gpu-scope fence), the rest at the end.  Breakdown and a failed earlier
+// tile keep the stage protocol going
 // with the arithmetic skipped, so no warp waits on a stage that never comes.
 constexpr int kPwCols = 8;                        // columns per tile (CT)
 // + a producer warpgroup (one active warp): 168 registers at launch, column
