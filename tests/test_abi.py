@@ -56,3 +56,20 @@ def test_library_is_sm100a():
         return
     out = subprocess.run([tool, "--list-elf", so], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_cascade_schedule_queries():
+    """Host-only queries of the 1-GPU cascade's schedule (no GPU needed): the
+    one-CTA cascade for m <= 64 when [Y|x] + A fit, else pivot blocks of 256
+    then 512 (cascade.cu run_cascade_impl)."""
+    from paper_1502_03543_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.pdas_cascade_one_cta(50, 200) == 1       # c1
+    assert lib.pdas_cascade_one_cta(64, 400) == 0       # [Y|x] + A > 200 KB
+    assert lib.pdas_cascade_one_cta(65, 100) == 0
+    assert lib.pdas_cascade_solve_block() == 256
+    assert lib.pdas_cascade_solve_blocks(50, 200) == 0  # one kernel
+    for n, nb in ((100, 1), (256, 1), (257, 2), (768, 2), (769, 3), (20000, 40),
+                  (100000, 196)):
+        assert lib.pdas_cascade_solve_blocks(2000, n) == nb, n
